@@ -1,0 +1,133 @@
+// common.cuh — shared plumbing for libsemidist_b200 (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <cmath>
+#include <cfloat>
+#include "../../include/semidist_b200.h"
+
+namespace sd {
+
+template <typename T>
+__host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+template <typename T>
+__host__ __device__ __forceinline__ T tmax(T a, T b) { return a < b ? b : a; }
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+
+struct Status {
+  int code;
+};
+
+#define SD_CUDA_TRY(expr)                                                        \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::sd::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+      return SD_E_CUDA;                                                          \
+    }                                                                            \
+  } while (0)
+
+#define SD_LAUNCH_CHECK()                                                        \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      ::sd::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));  \
+      return SD_E_CUDA;                                                          \
+    }                                                                            \
+  } while (0)
+
+#define SD_TRY(expr)                                                             \
+  do {                                                                           \
+    int _s = (expr);                                                             \
+    if (_s != SD_OK) return _s;                                                  \
+  } while (0)
+
+inline cudaStream_t as_stream(sd_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms();
+int64_t smem_optin_bytes();
+
+// Stream-ordered scratch allocation that is released when the guard dies
+// (the release is itself stream-ordered, so kernels already enqueued keep
+// a valid buffer).
+struct Scratch {
+  void* ptr = nullptr;
+  cudaStream_t stream = 0;
+  Scratch() = default;
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+  int alloc(size_t bytes, cudaStream_t s) {
+    stream = s;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&ptr, bytes, s);
+    if (e != cudaSuccess) {
+      ptr = nullptr;
+      set_error(std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+      return SD_E_CUDA;
+    }
+    return SD_OK;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
+// ----------------------------------------------------------- device utils
+template <typename T> struct Num;
+template <> struct Num<float> {
+  __device__ __forceinline__ static float inf() { return __int_as_float(0x7f800000); }
+  __device__ __forceinline__ static float big() { return __int_as_float(0x7f800000); }  // KL saturation (1e308 not representable)
+  __device__ __forceinline__ static float eps() { return FLT_EPSILON; }
+};
+template <> struct Num<double> {
+  __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000ULL); }
+  __device__ __forceinline__ static double big() { return 1e308; }  // KL_SATURATION, metrics.py:29
+  __device__ __forceinline__ static double eps() { return DBL_EPSILON; }
+};
+
+// Exact IEEE ops, spelled out so that no FMA contraction can change the
+// rounding relative to the numpy reference (the library is also compiled
+// with -fmad=false).
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float log_(float a) { return logf(a); }
+__device__ __forceinline__ double log_(double a) { return log(a); }
+__device__ __forceinline__ float pow_(float a, float b) { return powf(a, b); }
+__device__ __forceinline__ double pow_(double a, double b) { return pow(a, b); }
+__device__ __forceinline__ float abs_(float a) { return fabsf(a); }
+__device__ __forceinline__ double abs_(double a) { return fabs(a); }
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Murmur3 fmix32 (hashtable.py:21-29).
+__device__ __forceinline__ uint32_t mix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
+}  // namespace sd
+
+#define SD_DISPATCH_DTYPE(dt, T, ...)                                  \
+  [&]() -> int {                                                       \
+    if ((dt) == SD_F32) { using T = float; return __VA_ARGS__(); }     \
+    if ((dt) == SD_F64) { using T = double; return __VA_ARGS__(); }    \
+    ::sd::set_error("dtype must be SD_F32 or SD_F64");                 \
+    return SD_E_INVALID;                                               \
+  }()

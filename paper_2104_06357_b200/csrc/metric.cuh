@@ -1,0 +1,140 @@
+// metric.cuh — Table-1 catalog on device (metrics.py:102-270).
+//
+// expand_cell() is the element-wise epilogue of pairwise_distances_detail
+// (metrics.py:368-374): expansion (metrics.py:102-159) then post-scale
+// (metrics.py:162-180), written with the reference's operation order.
+//
+// For the fused intersection path (isect.cu) every (+)-reduced metric is
+// evaluated from intersecting columns only:
+//   dot family:  acc = Σ_{c∈A_i∩B_j} a·b                      (exact pass-1 value)
+//   kl:          acc = Σ_{c∈A_i∩B_j} a·log(a/b), cnt = |A_i∩B_j|; covered iff cnt == |A_i|
+//   NAMM (+):    union sum = S_A[i] + S_B[j] + Σ_{c∈A_i∩B_j} (⊗(a,b) − ⊗(a,0) − ⊗(0,b))
+//                with S_A[i] = Σ_c ⊗(a_ic,0), S_B[j] = Σ_c ⊗(0,b_jc)  (Eq. 5 union decomposition)
+#pragma once
+#include "common.cuh"
+#include "semiring.cuh"
+
+namespace sd {
+
+// NEGATIVE_RADICAND_TOLERANCE (metrics.py:27).  For a value obtained through a
+// cancelling reformulation or in fp32, the admissible rounding residue also
+// scales with the magnitude of the cancelled terms.
+template <typename T>
+__device__ __forceinline__ T clamp_radicand(T x, T scale, uint32_t& flags) {
+  const T tol = fmax(T(1e-9), T(64) * Num<T>::eps() * scale);
+  if (x < -tol) flags |= SD_FLAG_RADICAND;
+  return x < T(0) ? T(0) : x;
+}
+
+template <typename T>
+__device__ __forceinline__ T root_p(T x, T p) {
+  // numpy `x ** (1/p)` (metrics.py:166-172); 1/p == 0.5 and 1 hit numpy's exact fast paths
+  const T inv = div_rn(T(1), p);
+  if (inv == T(1)) return x;
+  if (inv == T(0.5)) return sqrt_rn(x);
+  return pow_(x, inv);
+}
+
+// Per-row statistics layout (s0, s1) for each metric, both sides:
+//   correlation: s0 = signed sum, s1 = l2sq     cosine: s0 = l2
+//   dice, jaccard: s0 = l0                        euclidean: s0 = l2sq
+//   kl (A side): s0 = l0 (coverage test)          NAMM (fused path): s0 = one-sided sum
+template <typename T>
+__device__ __forceinline__ T expand_cell(int metric, T d, T a0, T a1, T b0, T b1, T k, T p,
+                                         uint32_t& flags) {
+  switch (metric) {
+    case SD_M_CORRELATION: {  // metrics.py:121-132
+      T fa = clamp_radicand(sub_rn(mul_rn(k, a1), mul_rn(a0, a0)), mul_rn(k, a1), flags);
+      T fb = clamp_radicand(sub_rn(mul_rn(k, b1), mul_rn(b0, b0)), mul_rn(k, b1), flags);
+      T denom = sqrt_rn(mul_rn(fa, fb));
+      T num = sub_rn(mul_rn(k, d), mul_rn(a0, b0));
+      if (denom > T(0)) return sub_rn(T(1), div_rn(num, denom));
+      return (a1 == T(0) && b1 == T(0)) ? T(0) : T(1);
+    }
+    case SD_M_COSINE: {  // metrics.py:112-118
+      T denom = mul_rn(a0, b0);
+      if (denom > T(0)) return sub_rn(T(1), div_rn(d, denom));
+      return (a0 == T(0) && b0 == T(0)) ? T(0) : T(1);
+    }
+    case SD_M_DICE: {  // metrics.py:135-140
+      T denom = add_rn(a0, b0);
+      return denom > T(0) ? sub_rn(T(1), div_rn(mul_rn(T(2), d), denom)) : T(0);
+    }
+    case SD_M_DOT:  // metrics.py:102-103
+    case SD_M_KL:
+      return d;
+    case SD_M_EUCLIDEAN: {  // metrics.py:106-109 + _sqrt_post 162-163
+      T x = add_rn(sub_rn(a0, mul_rn(T(2), d)), b0);
+      return sqrt_rn(clamp_radicand(x, add_rn(a0, b0), flags));
+    }
+    case SD_M_HELLINGER:  // metrics.py:158-159
+      return sub_rn(T(1), sqrt_rn(clamp_radicand(d, T(1), flags)));
+    case SD_M_JACCARD: {  // metrics.py:143-149
+      T denom = sub_rn(add_rn(a0, b0), d);
+      if (denom > T(0)) return sub_rn(T(1), div_rn(d, denom));
+      return (a0 == T(0) && b0 == T(0)) ? T(0) : T(1);
+    }
+    case SD_M_RUSSELRAO:  // metrics.py:152-155
+      return k == T(0) ? T(0) : div_rn(sub_rn(k, d), k);
+    case SD_M_HAMMING:  // _mean_post, metrics.py:175-176
+      return k != T(0) ? div_rn(d, k) : T(0);
+    case SD_M_JENSENSHANNON:  // _js_post, metrics.py:179-180
+      return sqrt_rn(div_rn(clamp_radicand(d, T(0), flags), T(2)));
+    case SD_M_MINKOWSKI:  // _root_post, metrics.py:166-172
+      return root_p(d, p);
+    default:  // canberra, chebyshev, manhattan: identity
+      return d;
+  }
+}
+
+// ---- contributions of one intersecting column for the fused path
+enum ContribKind { C_MUL = 0, C_KL = 1, C_ABS = 2, C_ABSPOW = 3, C_CANBERRA = 4, C_MISMATCH = 5, C_JS = 6 };
+
+__host__ __device__ inline int metric_contrib(int metric) {
+  switch (metric) {
+    case SD_M_KL: return C_KL;
+    case SD_M_MANHATTAN: return C_ABS;
+    case SD_M_MINKOWSKI: return C_ABSPOW;
+    case SD_M_CANBERRA: return C_CANBERRA;
+    case SD_M_HAMMING: return C_MISMATCH;
+    case SD_M_JENSENSHANNON: return C_JS;
+    case SD_M_CHEBYSHEV: return -1;  // max-reduce: not decomposable, engine path
+    default: return C_MUL;
+  }
+}
+
+__host__ __device__ inline int contrib_semiring(int ck) {
+  switch (ck) {
+    case C_MUL: return SD_SR_DOT;
+    case C_KL: return SD_SR_KL_TERM;
+    case C_ABS: return SD_SR_ABS_DIFF;
+    case C_ABSPOW: return SD_SR_ABS_DIFF_POW;
+    case C_CANBERRA: return SD_SR_CANBERRA;
+    case C_MISMATCH: return SD_SR_MISMATCH;
+    default: return SD_SR_JS_TERM;
+  }
+}
+
+template <int CK, typename T>
+__device__ __forceinline__ T contrib(T a, T b, T p) {
+  if constexpr (CK == C_MUL) {
+    return mul_rn(a, b);
+  } else if constexpr (CK == C_KL) {
+    return product<SD_SR_KL_TERM, T>(a, b, p);
+  } else {
+    constexpr int SR = CK == C_ABS ? SD_SR_ABS_DIFF
+                     : CK == C_ABSPOW ? SD_SR_ABS_DIFF_POW
+                     : CK == C_CANBERRA ? SD_SR_CANBERRA
+                     : CK == C_MISMATCH ? SD_SR_MISMATCH : SD_SR_JS_TERM;
+    const T both = product<SR, T>(a, b, p);
+    const T left = product<SR, T>(a, T(0), p);
+    const T right = product<SR, T>(T(0), b, p);
+    return sub_rn(sub_rn(both, left), right);
+  }
+}
+
+__host__ __device__ inline bool is_namm(int metric) {
+  return metric >= SD_M_CANBERRA && metric <= SD_M_MINKOWSKI;
+}
+
+}  // namespace sd

@@ -1,0 +1,154 @@
+// prep.cu — per-row statistics and element-wise preparation kernels.
+//
+// Row reductions run one warp per row and accumulate SEQUENTIALLY in
+// ascending column order (lane 0's running value, fed 32 elements at a time
+// through shuffles).  The fused intersection kernel (isect.cu) accumulates
+// its per-cell dot products in the same ascending order, so ||a||^2 and
+// <a,a> are bitwise equal and self-distances of the expanded metrics come
+// out exactly 0, as they do in the reference (hard part 4).
+#include "common.cuh"
+#include "prep.cuh"
+#include "semiring.cuh"
+
+namespace sd {
+
+template <typename T, int KIND, int SR>
+__device__ __forceinline__ T stat_term(T v, T p) {
+  if constexpr (KIND == SD_STAT_L0) return T(1);
+  else if constexpr (KIND == SD_STAT_L1) return abs_(v);
+  else if constexpr (KIND == SD_STAT_L2 || KIND == SD_STAT_L2SQ) return mul_rn(v, v);
+  else if constexpr (KIND == SD_STAT_SUM) return v;
+  else if constexpr (KIND == STAT_ONESIDED_A) return product<SR, T>(v, T(0), p);
+  else return product<SR, T>(T(0), v, p);  // STAT_ONESIDED_B
+}
+
+template <typename T, int KIND, int SR>
+__global__ void row_stat_kernel(const int64_t* __restrict__ ptr, const T* __restrict__ val,
+                                int64_t n_rows, T p, T* __restrict__ out) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int64_t beg = ptr[r], end = ptr[r + 1];
+    T s = T(0);
+    if constexpr (KIND == SD_STAT_L0) {
+      s = T(end - beg);
+    } else {
+      for (int64_t base = beg; base < end; base += 32) {
+        const int64_t e = base + lane;
+        T t = e < end ? stat_term<T, KIND, SR>(val[e], p) : T(0);
+        const int cnt = int(tmin<int64_t>(32, end - base));
+        for (int k = 0; k < cnt; ++k) s = add_rn(s, __shfl_sync(0xffffffffu, t, k));
+      }
+      if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
+    }
+    if (lane == 0) out[r] = s;
+  }
+}
+
+template <typename T, int KIND, int SR>
+static int launch_stat(const sd_csr* m, T p, void* out, cudaStream_t st) {
+  if (m->n_rows == 0) return SD_OK;
+  int64_t warps = m->n_rows;
+  int blocks = int(tmin<int64_t>((warps * 32 + 255) / 256, int64_t(num_sms()) * 16));
+  row_stat_kernel<T, KIND, SR><<<blocks, 256, 0, st>>>(
+      m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out));
+  SD_LAUNCH_CHECK();
+  return SD_OK;
+}
+
+int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void* out,
+             cudaStream_t st) {
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    const T pp = T(p);
+    switch (kind) {
+      case SD_STAT_L0: return launch_stat<T, SD_STAT_L0, 0>(m, pp, out, st);
+      case SD_STAT_L1: return launch_stat<T, SD_STAT_L1, 0>(m, pp, out, st);
+      case SD_STAT_L2: return launch_stat<T, SD_STAT_L2, 0>(m, pp, out, st);
+      case SD_STAT_L2SQ: return launch_stat<T, SD_STAT_L2SQ, 0>(m, pp, out, st);
+      case SD_STAT_SUM: return launch_stat<T, SD_STAT_SUM, 0>(m, pp, out, st);
+      case STAT_ONESIDED_A:
+        return SD_DISPATCH_SEMIRING(semiring, SR, [&]() -> int { return launch_stat<T, STAT_ONESIDED_A, SR>(m, pp, out, st); });
+      case STAT_ONESIDED_B:
+        return SD_DISPATCH_SEMIRING(semiring, SR, [&]() -> int { return launch_stat<T, STAT_ONESIDED_B, SR>(m, pp, out, st); });
+      default:
+        set_error("unknown row statistic kind");
+        return SD_E_INVALID;
+    }
+  });
+}
+
+__global__ void coo_rows_kernel(const int64_t* __restrict__ ptr, int64_t n_rows,
+                                int64_t* __restrict__ rows) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_rows; r += nwarps)
+    for (int64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) rows[e] = r;
+}
+
+int csr_to_coo(const sd_csr* m, int64_t* rows, cudaStream_t st) {
+  if (m->n_rows == 0 || m->nnz == 0) return SD_OK;
+  int blocks = int(tmin<int64_t>((m->n_rows * 32 + 255) / 256, int64_t(num_sms()) * 16));
+  coo_rows_kernel<<<blocks, 256, 0, st>>>(m->indptr, m->n_rows, rows);
+  SD_LAUNCH_CHECK();
+  return SD_OK;
+}
+
+template <typename T>
+__global__ void negative_kernel(const T* __restrict__ v, int64_t n, uint32_t* flags) {
+  bool neg = false;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    neg |= v[e] < T(0);
+  if (__any_sync(0xffffffffu, neg) && lane_id() == 0) atomicOr(flags, SD_FLAG_NEGATIVE);
+}
+
+int check_nonnegative(const sd_csr* m, int dtype, uint32_t* flags, cudaStream_t st) {
+  if (m->nnz == 0) return SD_OK;
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    int blocks = int(tmin<int64_t>((m->nnz + 255) / 256, int64_t(num_sms()) * 8));
+    negative_kernel<T><<<blocks, 256, 0, st>>>(static_cast<const T*>(m->values), m->nnz, flags);
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  });
+}
+
+template <typename T>
+__global__ void sqrt_kernel(const T* __restrict__ v, int64_t n, T* __restrict__ out) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    out[e] = sqrt_rn(v[e]);
+}
+
+int sqrt_values(const sd_csr* m, int dtype, void* out, cudaStream_t st) {
+  if (m->nnz == 0) return SD_OK;
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    int blocks = int(tmin<int64_t>((m->nnz + 255) / 256, int64_t(num_sms()) * 8));
+    sqrt_kernel<T><<<blocks, 256, 0, st>>>(static_cast<const T*>(m->values), m->nnz,
+                                           static_cast<T*>(out));
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  });
+}
+
+template <typename T>
+__global__ void fill_kernel(T* __restrict__ out, int64_t m, int64_t n, int64_t ldo, T value) {
+  const int64_t total = m * n;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    out[i * ldo + j] = value;
+  }
+}
+
+int fill(void* out, int64_t m, int64_t n, int64_t ldo, int dtype, double value, cudaStream_t st) {
+  if (m == 0 || n == 0) return SD_OK;
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    int blocks = int(tmin<int64_t>((m * n + 255) / 256, int64_t(num_sms()) * 16));
+    fill_kernel<T><<<blocks, 256, 0, st>>>(static_cast<T*>(out), m, n, ldo, T(value));
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  });
+}
+
+}  // namespace sd

@@ -1,0 +1,52 @@
+// prep.cuh — internal entry points shared by the translation units.
+#pragma once
+#include "common.cuh"
+
+namespace sd {
+
+struct Stats {  // per-row statistics the metric epilogue reads (metric.cuh layout)
+  const void* s[3] = {nullptr, nullptr, nullptr};
+};
+
+// internal statistic kinds beyond sd_stat_kind: one-sided NAMM sums
+//   S_A[i] = sum_c ⊗(a_ic, 0)   and   S_B[j] = sum_c ⊗(0, b_jc)
+constexpr int STAT_ONESIDED_A = 16;
+constexpr int STAT_ONESIDED_B = 17;
+
+int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void* out,
+             cudaStream_t st);
+int csr_to_coo(const sd_csr* m, int64_t* rows, cudaStream_t st);
+int check_nonnegative(const sd_csr* m, int dtype, uint32_t* flags, cudaStream_t st);
+int sqrt_values(const sd_csr* m, int dtype, void* out, cudaStream_t st);
+int fill(void* out, int64_t m, int64_t n, int64_t ldo, int dtype, double value, cudaStream_t st);
+
+// engine.cu
+int engine_pass(const sd_csr* a, const sd_csr* b, int dtype, int semiring, double p, int pass,
+                const sd_strategy* strategy, void* out, int64_t ldo, sd_report* report,
+                cudaStream_t st);
+void reference_report(const int64_t* degrees, int64_t n_rows, const sd_strategy* strategy,
+                      int64_t swept_nnz, sd_report* rep);
+
+// epilogue.cu
+int metric_stats(const sd_csr* m, int dtype, const sd_metric_desc* md, bool a_side, void* buf,
+                 Stats* out, cudaStream_t st);
+int64_t metric_stats_count(int metric);
+int expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd_metric_desc* md,
+           int64_t n_cols, const Stats& sa, const Stats& sb, const void* miss,
+           uint32_t* flags, cudaStream_t st);
+
+int metric_semiring(int metric);
+int default_tile(int dtype);
+int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream_t st);
+int isect_stats(const sd_csr* a, const sd_csr* b, int dtype, const sd_metric_desc* md, Scratch& sa_buf,
+                Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st);
+int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
+              const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
+              void* out_d, int64_t* out_i, uint32_t* flags, cudaStream_t st);
+int topk_rows(const void* dist, int64_t m, int64_t n, int64_t ldd, int dtype, int k, int64_t base,
+              void* od, int64_t* oi, cudaStream_t st);
+int topk_merge(const void* cd, const int64_t* ci, int64_t m, int lists, int k, int dtype, void* od,
+               int64_t* oi, cudaStream_t st);
+bool metric_two_pass(int metric);
+
+}  // namespace sd

@@ -1,0 +1,299 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Every test calls libsemidist_b200.so; the comparison target is the golden
+vectors produced by the reference itself and, for sizes the fixtures do not
+hold, the oracle (oracle/semidist_oracle.py, pinned bitwise to the reference
+by tests/test_oracle_golden.py).  Tolerance rule: tests/parity.py.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2104_06357_b200 as sd
+from golden_cases import csr
+from oracle import semidist_oracle as O
+from parity import assert_knn_parity, assert_parity
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = [np.float64, np.float32]
+
+
+def _strategy(s):
+    if isinstance(s, list):
+        return sd.ExecutionStrategy(sd.StrategyKind.BALANCED_HASH, accumulator_capacity=s[1], max_load_factor=s[2])
+    return s
+
+
+def _f32(m):
+    return m.with_values(np.asarray(m.values, dtype=np.float32).astype(np.float64))
+
+
+def _host(m):
+    return sd.CsrMatrix(m.n_rows, m.n_cols, m.indptr, m.indices, m.values)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2104_06357_b200 import _lib
+    _lib.load()
+
+
+# ------------------------------------------------------------ golden vectors
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_golden_pairwise_fused_and_engine(golden, dtype):
+    """All 15 metrics x {auto (fused), dense, hash(8/16), naive} vs the reference's outputs."""
+    cases, arrays = golden
+    n = 0
+    for c in cases:
+        if c["kind"] != "pairwise":
+            continue
+        a, b = _host(csr(arrays, c["a"])), _host(csr(arrays, c["b"]))
+        if dtype == np.float32 and not (np.asarray(a.values, np.float32) == a.values).all():
+            a, b = _f32(a), _f32(b)
+            ref = O.pairwise_distances(a, b, c["metric"], p=c["p"], strict=c["strict"])
+        else:
+            ref = arrays[c["id"] + ".out"]
+        spec = sd.metric_registry(c["metric"], p=c["p"], strict=c["strict"])
+        got, rep, _ = sd.pairwise_distances_detail(a, b, spec, _strategy(c["strategy"]), dtype=dtype)
+        assert got.dtype == np.float64 and got.flags["C_CONTIGUOUS"]
+        assert_parity(got, ref, a, b, c["metric"], dtype, p=c["p"], what=c["id"])
+        assert [rep.peak_accumulator_entries, rep.workspace_elements, rep.chunks_executed] == c["report"], c["id"]
+        n += 1
+    assert n > 100
+
+
+@pytest.mark.parametrize("strategy", [None, "dense", "hash", "naive"])
+def test_golden_pairwise_all_strategies_fp64(golden, strategy):
+    cases, arrays = golden
+    for c in cases:
+        if c["kind"] != "pairwise" or c["id"].startswith("zipf"):
+            continue
+        a, b = _host(csr(arrays, c["a"])), _host(csr(arrays, c["b"]))
+        spec = sd.metric_registry(c["metric"], p=c["p"], strict=c["strict"])
+        got = sd.pairwise_distances(a, b, spec, strategy)
+        assert_parity(got, arrays[c["id"] + ".out"], a, b, c["metric"], np.float64, p=c["p"],
+                      what=f"{c['id']}/{strategy}")
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_golden_generalized(golden, dtype):
+    cases, arrays = golden
+    rings = {"dot": sd.dot_product(), "abs-diff": sd.absolute_difference(),
+             "abs-diff-max": sd.max_absolute_difference(), "canberra-ratio": sd.canberra_ratio(),
+             "mismatch": sd.mismatch_indicator(), "jensen-shannon-term": sd.jensen_shannon_term(),
+             "min-plus": sd.tropical_min_plus(), "abs-diff-pow": sd.absolute_difference_power(1.5)}
+    for c in cases:
+        if c["kind"] != "generalized":
+            continue
+        a, b = _host(csr(arrays, c["a"])), _host(csr(arrays, c["b"]))
+        ref = arrays[c["id"] + ".out"]
+        if dtype == np.float32:
+            a, b = _f32(a), _f32(b)
+            ref = O.generalized(a, b, c["ring"], p=1.5 if c["ring"] == "abs-diff-pow" else None)
+        for strat in (None, "naive", sd.ExecutionStrategy(sd.StrategyKind.BALANCED_HASH, 8)):
+            got, _ = sd.pairwise_generalized(a, b, rings[c["ring"]], strat, dtype=dtype)
+            if c["ring"] in ("min-plus", "abs-diff-max") and dtype == np.float64:
+                np.testing.assert_array_equal(got, ref, err_msg=c["id"])   # exact semirings
+            else:
+                rtol = 1e-12 if dtype == np.float64 else 1e-5
+                np.testing.assert_allclose(got, ref, rtol=rtol, atol=rtol * 30, err_msg=c["id"])
+
+
+def test_appendix_golden_exact():
+    a = sd.from_dense([[1.0, 0.0, 1.0]])
+    b = sd.from_dense([[0.0, 1.0, 0.0]])
+    spec = sd.metric_registry("manhattan")
+    for strategy in (None, "dense", "naive"):
+        assert sd.pairwise_distances(a, b, spec, strategy)[0, 0] == 3.0
+    out = sd.allocate_output(a, b, spec.semiring)
+    sd.pairwise_spmv_pass1(a, b, spec.semiring, sd.ExecutionStrategy(sd.StrategyKind.BALANCED_DENSE), out)
+    assert out[0, 0] == 1.0
+    sd.pairwise_spmv_pass2(a, b, spec.semiring, sd.ExecutionStrategy(sd.StrategyKind.BALANCED_DENSE), out)
+    assert out[0, 0] == 3.0
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_golden_knn(golden, dtype):
+    cases, arrays = golden
+    for c in cases:
+        if c["kind"] != "knn":
+            continue
+        q, ix = _host(csr(arrays, c["a"])), _host(csr(arrays, c["b"]))
+        spec = sd.metric_registry(c["metric"])
+        res = sd.kneighbors(ix, q, c["k"], spec, dtype=dtype)
+        full = O.pairwise_distances(q, ix, c["metric"])
+        tol = 1e-12 if dtype == np.float64 else 1e-5
+        assert_knn_parity(res.distances, res.indices, arrays[c["id"] + ".dist"], arrays[c["id"] + ".idx"],
+                          full, tol=tol * 10)
+        if dtype == np.float64:   # forced engine strategy + sd_topk_rows route
+            res2 = sd.kneighbors(ix, q, c["k"], spec, strategy="dense", batch_rows=7)
+            assert_knn_parity(res2.distances, res2.indices, arrays[c["id"] + ".dist"],
+                              arrays[c["id"] + ".idx"], full, tol=tol * 10)
+
+
+# ------------------------------------------------------------ reference test strategy, on GPU
+
+def test_self_distance_exact_zero():
+    """Norm and dot accumulate in the same order: euclidean/cosine self-distance is exactly 0
+    (as in the reference, metrics.py:106-118)."""
+    x = _host(sd.generate(sd.GenSpec(300, 5000, "zipf", zipf_s=1.3, zipf_max_degree=400, seed=4)))
+    for dtype in DTYPES:
+        for name in ("euclidean", "manhattan", "canberra", "hamming", "chebyshev", "jensenshannon"):
+            d = sd.pairwise_distances(x, x, sd.metric_registry(name), dtype=dtype)
+            if name in ("euclidean", "chebyshev", "hamming"):
+                assert np.all(np.diag(d) == 0.0), (name, dtype)
+            else:
+                assert np.abs(np.diag(d)).max() <= (1e-9 if dtype == np.float64 else 1e-3), (name, dtype)
+
+
+def test_kl_strict_and_permissive():
+    a = sd.from_dense([[0.5, 0.5]])
+    b = sd.from_dense([[1.0, 0.0]])
+    with pytest.raises(sd.DomainError):
+        sd.pairwise_distances(a, b, sd.metric_registry("kl"))
+    assert sd.pairwise_distances(a, b, sd.metric_registry("kl", strict=False))[0, 0] == 1e308
+    with pytest.raises(sd.DomainError):
+        sd.pairwise_distances(a, b, sd.metric_registry("kl"), "dense")
+    d32 = sd.pairwise_distances(a, b, sd.metric_registry("kl", strict=False), dtype=np.float32)
+    assert np.isinf(d32[0, 0])
+
+
+def test_domain_errors():
+    neg = sd.from_dense([[-1.0, 0.5]])
+    pos = sd.from_dense([[1.0, 0.5]])
+    for name in ("kl", "jensenshannon", "hellinger"):
+        with pytest.raises(sd.DomainError):
+            sd.pairwise_distances(neg, pos, sd.metric_registry(name))
+        with pytest.raises(sd.DomainError):
+            sd.pairwise_distances(pos, neg, sd.metric_registry(name))
+    with pytest.raises(sd.DimensionMismatch):
+        sd.pairwise_distances(sd.from_dense([[1.0, 0.0]]), sd.from_dense([[1.0, 0, 0]]), sd.metric_registry("cosine"))
+
+
+def test_expansion_apply_hand_cases():
+    spec = sd.metric_registry("euclidean")
+    na = [sd.NormVector(sd.NormKind.L2_SQUARED, np.array([2.0]))]
+    nb = [sd.NormVector(sd.NormKind.L2_SQUARED, np.array([1.0]))]
+    np.testing.assert_allclose(sd.expansion_apply(np.array([[1.0]]), na, nb, spec, n_cols=2), [[1.0]])
+    norms = [sd.NormVector(sd.NormKind.L2_SQUARED, np.array([1.0]))]
+    with pytest.raises(sd.DomainError):
+        sd.expansion_apply(np.array([[10.0]]), norms, norms, spec, n_cols=2)
+    np.testing.assert_array_equal(
+        sd.expansion_apply(np.array([[1.0 + 2e-10]]), norms, norms, spec, n_cols=2), [[0.0]])
+    jn = [sd.NormVector(sd.NormKind.L0, np.array([3.0]))]
+    np.testing.assert_allclose(sd.expansion_apply(np.array([[3.0]]), jn, jn, sd.metric_registry("jaccard"),
+                                                  n_cols=8), [[0.0]])
+
+
+def test_determinism_bitwise():
+    x = _host(sd.generate(sd.GenSpec(200, 3000, "zipf", zipf_s=1.3, zipf_max_degree=500, seed=9)))
+    for name, strat in [("cosine", None), ("manhattan", None), ("canberra", "dense"), ("chebyshev", None),
+                        ("manhattan", sd.ExecutionStrategy(sd.StrategyKind.BALANCED_HASH, 16))]:
+        d1 = sd.pairwise_distances(x, x, sd.metric_registry(name), strat, dtype=np.float32)
+        d2 = sd.pairwise_distances(x, x, sd.metric_registry(name), strat, dtype=np.float32)
+        np.testing.assert_array_equal(d1, d2)
+
+
+def test_knn_batching_invariance_and_ties():
+    x = _host(sd.generate(sd.GenSpec(400, 300, "zipf", zipf_s=1.1, zipf_max_degree=150, seed=8)))
+    spec = sd.metric_registry("cosine")
+    base = sd.kneighbors(x, x, 10, spec, batch_rows=400)
+    for rows in (1, 64, 117):
+        r = sd.kneighbors(x, x, 10, spec, batch_rows=rows)
+        np.testing.assert_array_equal(r.indices, base.indices)
+        np.testing.assert_array_equal(r.distances, base.distances)
+    ref_d, ref_i = O.kneighbors(x, x, 10, "cosine")
+    full = O.pairwise_distances(x, x, "cosine")
+    assert_knn_parity(base.distances, base.indices, ref_d, ref_i, full, tol=1e-11)
+    with pytest.raises(sd.KTooLarge):
+        sd.kneighbors(x, x, 401, spec)
+    vals, idx = sd.select_topk([1.0, 1.0, 1.0], 2)
+    assert idx.tolist() == [0, 1]
+    vals, idx = sd.select_topk([3.0, 1.0, 2.0], 2)
+    assert idx.tolist() == [1, 2] and vals.tolist() == [1.0, 2.0]
+
+
+def test_knn_large_k_and_chebyshev_routes():
+    x = _host(sd.generate(sd.GenSpec(300, 200, "zipf", zipf_s=1.3, zipf_max_degree=60, seed=18)))
+    for name, k in (("cosine", 150), ("chebyshev", 12), ("manhattan", 64)):
+        res = sd.kneighbors(x, sd.slice_rows(x, 0, 40), k, sd.metric_registry(name))
+        ref_d, ref_i = O.kneighbors(x, O.Csr.of(x).slice(0, 40), k, name)
+        full = O.pairwise_distances(O.Csr.of(x).slice(0, 40), x, name)
+        assert_knn_parity(res.distances, res.indices, ref_d, ref_i, full, tol=1e-11)
+
+
+def test_hash_chunking_forced_and_reported():
+    """Degrees above 50% of a tiny capacity force column chunking (test_engine.py:294-303)."""
+    rng = np.random.default_rng(12)
+    a = sd.from_dense(np.where(rng.random((20, 60)) < 0.5, rng.uniform(0.1, 1, (20, 60)), 0.0))
+    b = sd.from_dense(np.where(rng.random((10, 60)) < 0.3, rng.uniform(0.1, 1, (10, 60)), 0.0))
+    strat = sd.ExecutionStrategy(sd.StrategyKind.BALANCED_HASH, accumulator_capacity=16, max_load_factor=0.5)
+    for ring in (sd.absolute_difference(), sd.max_absolute_difference(), sd.tropical_min_plus()):
+        out, rep = sd.pairwise_generalized(a, b, ring, strat)
+        assert rep.peak_accumulator_entries <= 8 and rep.chunks_executed > a.n_rows
+        base = O.generalized(a, b, ring.name)
+        np.testing.assert_allclose(out, base, rtol=1e-12, atol=1e-12)
+
+
+def test_empty_and_degenerate_shapes():
+    spec = sd.metric_registry("manhattan")
+    z = sd.validate_and_canonicalize([0], [], [], n_cols=5)
+    x = sd.from_dense([[0.0, 1.0, 0, 0, 2.0]])
+    assert sd.pairwise_distances(z, x, spec).shape == (0, 1)
+    assert sd.pairwise_distances(x, z, spec).shape == (1, 0)
+    e = sd.validate_and_canonicalize([0, 0, 0], [], [], n_cols=5)
+    for name in sd.METRIC_NAMES:
+        p = 2.0 if name == "minkowski" else None
+        d = sd.pairwise_distances(e, x, sd.metric_registry(name, p=p, strict=False))
+        ref = O.pairwise_distances(e, x, name, p=p, strict=False)
+        np.testing.assert_allclose(d, ref, rtol=1e-12, atol=1e-12, err_msg=name)
+
+
+# ------------------------------------------------------------ full-size configs
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_config1_full_vs_oracle(dtype):
+    """BASELINE config 1 at full size (1k x 1k, 10k cols, 1% density), manhattan + cosine."""
+    A = _f32(sd.generate(sd.GenSpec(1000, 10000, "uniform", degree=100, seed=1)))
+    B = _f32(sd.generate(sd.GenSpec(1000, 10000, "uniform", degree=100, seed=2)))
+    for name in ("manhattan", "cosine"):
+        ref = O.pairwise_distances(A, B, name)
+        for strategy in (None, "dense"):
+            got = sd.pairwise_distances(A, B, sd.metric_registry(name), strategy, dtype=dtype)
+            assert_parity(got, ref, A, B, name, dtype, what=f"C1/{name}/{strategy}")
+
+
+def test_power_law_properties_at_scale():
+    """MovieLens-shaped (config 2) index: size-independent properties on a full-size
+    index — self-distance, symmetry of the self block, expanded vs two-pass euclidean,
+    and oracle parity on a sampled block."""
+    idx = _f32(sd.generate(sd.GenSpec(162541, 59047, "zipf", zipf_s=1.5, zipf_max_degree=32000, seed=25)))
+    rng = np.random.default_rng(26)
+    rows = np.sort(rng.choice(idx.n_rows, 64, replace=False))
+    q = _gather_rows(idx, rows)
+    d = sd.pairwise_distances(q, idx, sd.metric_registry("cosine"), dtype=np.float32)
+    assert d.shape == (64, idx.n_rows)
+    np.testing.assert_allclose(d[np.arange(64), rows], 0.0, atol=1e-6)
+    cols = np.sort(rng.choice(idx.n_rows, 2000, replace=False))
+    sub = _gather_rows(idx, cols)
+    ref = O.pairwise_distances(q, sub, "cosine")
+    assert_parity(d[:, cols], ref, q, sub, "cosine", np.float32, what="C2 sample")
+    e = sd.pairwise_distances(q, sub, sd.metric_registry("euclidean"), dtype=np.float64)
+    m2 = sd.pairwise_distances(q, sub, sd.metric_registry("minkowski", p=2.0), dtype=np.float64)
+    np.testing.assert_allclose(e, m2, rtol=1e-9, atol=1e-9)
+
+
+def _gather_rows(m, rows):
+    ptr = np.asarray(m.indptr)
+    parts_i, parts_v, newptr = [], [], [0]
+    for r in rows:
+        lo, hi = ptr[r], ptr[r + 1]
+        parts_i.append(np.asarray(m.indices[lo:hi]))
+        parts_v.append(np.asarray(m.values[lo:hi]))
+        newptr.append(newptr[-1] + hi - lo)
+    return sd.CsrMatrix(len(rows), m.n_cols, np.asarray(newptr, dtype=np.int64),
+                        np.concatenate(parts_i), np.concatenate(parts_v))
