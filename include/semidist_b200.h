@@ -137,6 +137,8 @@ typedef struct sd_index sd_index; /* opaque J-blocked inverted index of B */
 /* ---------------------------------------------------------------- misc */
 SD_API int sd_version(void);
 SD_API const char* sd_last_error(void);
+/* Cumulative number of kernels this library has launched in the process. */
+SD_API uint64_t sd_launch_count(void);
 /* Largest dynamic shared memory per block on `device` (opt-in), bytes. */
 SD_API int sd_smem_budget(int device, int64_t* bytes);
 

@@ -68,6 +68,7 @@ _CSR = ctypes.POINTER(SdCsr)
 SIGNATURES = [
     ("sd_version", _I, []),
     ("sd_last_error", ctypes.c_char_p, []),
+    ("sd_launch_count", ctypes.c_uint64, []),
     ("sd_smem_budget", _I, [_I, ctypes.POINTER(_I64)]),
     ("sd_row_stat", _I, [_CSR, _I, _I, _P, _P]),
     ("sd_csr_to_coo", _I, [_CSR, _P, _P]),
@@ -175,6 +176,15 @@ def metric_struct(name, p=None, strict=True, pre_transformed=False):
 def new_flags(device):
     import torch
     return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def any_negative(d):
+    """True if any stored value of a DeviceCsr is negative (one 4-byte D2H)."""
+    flags = new_flags(d.device)
+    csr = csr_struct(d)
+    check(load().sd_check_nonnegative(ctypes.byref(csr), dtype_code(d.dtype), flags.data_ptr(),
+                                      stream_handle(d.device)), "sd_check_nonnegative")
+    return bool(int(flags.item()) & SD_FLAG_NEGATIVE)
 
 
 def transform_values(d, transform):

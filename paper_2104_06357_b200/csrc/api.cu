@@ -3,6 +3,7 @@
 // Orchestration mirrors pairwise_distances_detail (metrics.py:320-375) and
 // kneighbors_detail (knn.py:50-82); every piece of arithmetic runs in the
 // kernels of prep.cu / engine.cu / isect.cu / epilogue.cu / topk.cu.
+#include <atomic>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -15,6 +16,8 @@ namespace sd {
 
 static thread_local std::string g_error;
 void set_error(const std::string& msg) { g_error = msg; }
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int num_sms() {
   int dev = 0, n = 148;
@@ -170,6 +173,7 @@ using namespace sd;
 extern "C" {
 
 int sd_version(void) { return SD_ABI_VERSION; }
+uint64_t sd_launch_count(void) { return g_launches.load(); }
 const char* sd_last_error(void) { return g_error.c_str(); }
 
 int sd_smem_budget(int device, int64_t* bytes) {

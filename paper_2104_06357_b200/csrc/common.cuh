@@ -16,6 +16,7 @@ __host__ __device__ __forceinline__ T tmax(T a, T b) { return a < b ? b : a; }
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string& msg);
+void count_launch();
 
 struct Status {
   int code;
@@ -32,9 +33,11 @@ struct Status {
 
 #define SD_LAUNCH_CHECK()                                                        \
   do {                                                                           \
+    ::sd::count_launch();                                                        \
     cudaError_t _e = cudaGetLastError();                                         \
     if (_e != cudaSuccess) {                                                     \
-      ::sd::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));  \
+      ::sd::set_error(std::string("kernel launch (") + __FILE__ + ":" +          \
+                      std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \
       return SD_E_CUDA;                                                          \
     }                                                                            \
   } while (0)
@@ -49,6 +52,34 @@ inline cudaStream_t as_stream(sd_stream_t s) { return reinterpret_cast<cudaStrea
 
 int num_sms();
 int64_t smem_optin_bytes();
+
+// Opt a kernel into `dyn` bytes of dynamic shared memory, accounting for its
+// static shared memory; reports the kernel name on failure.
+template <typename K>
+int prepare_smem(K kernel, size_t dyn, const char* name) {
+  cudaFuncAttributes attr{};
+  cudaError_t e = cudaFuncGetAttributes(&attr, kernel);
+  if (e != cudaSuccess) {
+    set_error(std::string(name) + ": cudaFuncGetAttributes: " + cudaGetErrorString(e));
+    return SD_E_CUDA;
+  }
+  if (int64_t(dyn + attr.sharedSizeBytes) > smem_optin_bytes()) {
+    set_error(std::string(name) + ": shared memory request exceeds the opt-in limit");
+    return SD_E_INVALID;
+  }
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+  if (e != cudaSuccess) {
+    set_error(std::string(name) + ": cudaFuncSetAttribute(" + std::to_string(dyn) + "): " + cudaGetErrorString(e));
+    return SD_E_CUDA;
+  }
+  return SD_OK;
+}
+
+inline int64_t static_smem(const void* kernel) {
+  cudaFuncAttributes attr{};
+  if (cudaFuncGetAttributes(&attr, kernel) != cudaSuccess) return 0;
+  return int64_t(attr.sharedSizeBytes);
+}
 
 // Stream-ordered scratch allocation that is released when the guard dies
 // (the release is itself stream-ordered, so kernels already enqueued keep

@@ -277,9 +277,8 @@ static int next_pow2(int64_t x) {
 template <typename T, int SR, int PASS>
 static int run_classes(std::vector<LaunchClass>& classes, const sd_csr* staged, const sd_csr* swept,
                        double p, void* out, int64_t ldo, cudaStream_t st) {
-  const int64_t optin = smem_optin_bytes();
+  const int64_t optin = smem_optin_bytes() - static_smem((const void*)pass_kernel<T, SR, PASS>);
   const int sms = num_sms();
-  cudaFuncSetAttribute(pass_kernel<T, SR, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(optin));
   for (auto& cls : classes) {
     if (cls.units.empty()) continue;
     const int64_t per_slot = cls.hash ? int64_t(cls.slot) * (4 + sizeof(T)) + 16 : int64_t(cls.slot) * sizeof(T);
@@ -309,6 +308,7 @@ static int run_classes(std::vector<LaunchClass>& classes, const sd_csr* staged, 
     SD_CUDA_TRY(cudaMemcpyAsync(db.ptr, boff.data(), sizeof(int64_t) * boff.size(), cudaMemcpyHostToDevice, st));
     const size_t smem = cls.hash ? ((size_t(R) * cls.slot * 4 + 15) & ~size_t(15)) + size_t(R) * cls.slot * sizeof(T)
                                  : size_t(R) * cls.slot * sizeof(T);
+    SD_TRY(prepare_smem(pass_kernel<T, SR, PASS>, smem, "pass_kernel"));
     const int per_sm = std::max<int>(1, int(std::min<int64_t>(8, (228 * 1024) / int64_t(smem + 2048))));
     const int64_t target = int64_t(sms) * per_sm * 2;
     int64_t ny = std::max<int64_t>(1, (target + nb - 1) / nb);

@@ -269,14 +269,14 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
 
 template <typename T, int CK, int KPL>
 static int launch_isect(IsectArgs<T>& args, cudaStream_t st) {
-  const int64_t optin = smem_optin_bytes();
+  const int64_t optin = smem_optin_bytes() - static_smem((const void*)isect_kernel<T, CK, KPL>);
   const int64_t per_warp = int64_t(args.tile) * sizeof(T) * (CK == C_KL ? 2 : 1);
   int W = int(std::min<int64_t>(16, (optin - 1024) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const size_t smem = size_t(W) * per_warp;
-  cudaFuncSetAttribute(isect_kernel<T, CK, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  SD_TRY(prepare_smem(isect_kernel<T, CK, KPL>, smem, "isect_kernel"));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, isect_kernel<T, CK, KPL>, W * 32, smem);
+  SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, isect_kernel<T, CK, KPL>, W * 32, smem));
   per_sm = std::max(1, per_sm);
   const int64_t warps_needed = args.m;
   int64_t blocks = std::min<int64_t>(int64_t(num_sms()) * per_sm, (warps_needed + W - 1) / W);
@@ -286,36 +286,37 @@ static int launch_isect(IsectArgs<T>& args, cudaStream_t st) {
   return SD_OK;
 }
 
-__global__ void degree_keys_kernel(const int64_t* __restrict__ ptr, int64_t m, int32_t* keys, int32_t* vals) {
-  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < m; r += int64_t(gridDim.x) * blockDim.x) {
-    keys[r] = int32_t(tmin<int64_t>(ptr[r + 1] - ptr[r], INT32_MAX));
-    vals[r] = int32_t(r);
+// Query schedule: rows ordered by descending floor(log2(degree)) so the
+// dynamic queue hands out the longest rows first (LPT).  One CTA: bucket
+// histogram, scan, scatter — no library sort in the hot path.
+__global__ void __launch_bounds__(1024) degree_order_kernel(const int64_t* __restrict__ ptr, int64_t m,
+                                                            int32_t* __restrict__ order) {
+  __shared__ unsigned int hist[64];
+  __shared__ unsigned int base[64];
+  if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
+    const int64_t d = ptr[r + 1] - ptr[r];
+    const int b = d > 0 ? 63 - __clzll(d) : 0;   // floor(log2 d)
+    atomicAdd(&hist[63 - b], 1u);                // descending degree
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int acc = 0;
+    for (int b = 0; b < 64; ++b) { base[b] = acc; acc += hist[b]; }
+  }
+  __syncthreads();
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
+    const int64_t d = ptr[r + 1] - ptr[r];
+    const int b = d > 0 ? 63 - __clzll(d) : 0;
+    order[atomicAdd(&base[63 - b], 1u)] = int32_t(r);
   }
 }
 
-int fill_degree_keys(const int64_t* ptr, int64_t m, int32_t* keys, int32_t* vals, cudaStream_t st) {
-  const int blocks = int(std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 8));
-  degree_keys_kernel<<<std::max(1, blocks), 256, 0, st>>>(ptr, m, keys, vals);
-  SD_LAUNCH_CHECK();
-  return SD_OK;
-}
-
-// Queries sorted by degree, longest first (a dynamic queue then balances).
 static int degree_order(const sd_csr* a, cudaStream_t st, Scratch& order_buf) {
-  const int64_t m = a->n_rows;
-  Scratch keys, keys_out, vals;
-  SD_TRY(order_buf.alloc(sizeof(int32_t) * m, st));
-  SD_TRY(keys.alloc(sizeof(int32_t) * m, st));
-  SD_TRY(keys_out.alloc(sizeof(int32_t) * m, st));
-  SD_TRY(vals.alloc(sizeof(int32_t) * m, st));
-  SD_TRY(fill_degree_keys(a->indptr, m, keys.as<int32_t>(), vals.as<int32_t>(), st));
-  size_t tb = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys.as<int32_t>(), keys_out.as<int32_t>(),
-                                            vals.as<int32_t>(), order_buf.as<int32_t>(), int(m), 0, 32, st);
-  Scratch tmp;
-  SD_TRY(tmp.alloc(tb, st));
-  SD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.ptr, tb, keys.as<int32_t>(), keys_out.as<int32_t>(),
-                                                        vals.as<int32_t>(), order_buf.as<int32_t>(), int(m), 0, 32, st));
+  SD_TRY(order_buf.alloc(sizeof(int32_t) * std::max<int64_t>(1, a->n_rows), st));
+  degree_order_kernel<<<1, 1024, 0, st>>>(a->indptr, a->n_rows, order_buf.as<int32_t>());
+  SD_LAUNCH_CHECK();
   return SD_OK;
 }
 

@@ -202,13 +202,15 @@ def _engine_report(da, db, spec_passes, name, strategy, a, b):
 
 
 def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=np.float64, device=None,
-                              return_device=False, check_flags=True):
+                              return_device=False, check_flags=True, out=None):
     """Distances + WorkspaceReport + per-phase device times (metrics.py:320-375).
 
     ``strategy`` None/"auto" runs the fused intersection kernel (two-pass
     engine for chebyshev); "naive"/"dense"/"hash"/ExecutionStrategy force the
     engine with the reference's chunking semantics.  ``workers`` is accepted
-    for compatibility and ignored.
+    for compatibility and ignored.  ``out`` (host numpy array or CPU torch
+    tensor, ideally pinned, shape (m, n)) receives the result by one
+    device->host copy and is returned instead of a new array.
     """
     import torch
     if a.n_cols != b.n_cols:
@@ -221,6 +223,7 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
     passes = getattr(spec, "passes", 2 if name in METRIC_NAMES[9:] else 1)
     fused = strategy is None or (isinstance(strategy, str) and strategy == "auto")
     report = _engine_report(da, db, passes, name, strategy, a, b)
+    host_out = out
     out = torch.empty((a.n_rows, b.n_rows), dtype=tdt, device=da.device)
     flags = _lib.new_flags(da.device)
     md = _lib.metric_struct(name, p, strict, pre_transformed=transform is not None)
@@ -242,6 +245,14 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
         _lib.raise_flags(int(flags.item()), name)
     timings = {"norms": phases[0] / 1e3, "pass1": phases[1] / 1e3, "pass2": phases[2] / 1e3,
                "expansion": phases[3] / 1e3}
+    if host_out is not None:
+        dst = host_out if isinstance(host_out, torch.Tensor) else torch.from_numpy(host_out)
+        if tuple(dst.shape) != (a.n_rows, b.n_rows):
+            raise ValueError(f"out has shape {tuple(dst.shape)}, expected {(a.n_rows, b.n_rows)}")
+        src = out if dst.dtype == out.dtype else out.to(dst.dtype)
+        dst.copy_(src, non_blocking=dst.is_pinned())
+        torch.cuda.current_stream(da.device).synchronize()
+        return host_out, report, timings
     if return_device:
         return out, report, timings
     return _lib.as_numpy_f64(out), report, timings

@@ -308,13 +308,16 @@ def to_device(m, dtype="float64", device=None, transform=None):
         raise ValueError("column ids must fit in int32 on device")
     d = DeviceCsr(
         int(m.n_rows), int(m.n_cols),
-        torch.from_numpy(indptr).to(dev, non_blocking=False),
-        torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int32)).to(dev),
-        torch.from_numpy(np.ascontiguousarray(m.values, dtype=np.float64)).to(dev).to(tdtype),
+        torch.from_numpy(np.array(indptr, dtype=np.int64, copy=True)).to(dev),
+        torch.from_numpy(np.array(indices, dtype=np.int32, copy=True)).to(dev),
+        torch.from_numpy(np.array(m.values, dtype=np.float64, copy=True)).to(dev).to(tdtype),
     )
     d._host_degrees = np.diff(indptr)
     if transform is not None:
         from . import _lib
+        from .errors import DomainError
+        if _lib.any_negative(d):   # domain check on the raw values (metrics.py:308-311)
+            raise DomainError("hellinger requires non-negative inputs")
         d = _lib.transform_values(d, transform)
     per[key] = d
     return d
@@ -330,3 +333,26 @@ def _torch_dtype(dtype):
     if name == "float64":
         return torch.float64
     raise ValueError(f"unsupported value dtype {dtype!r}; use float32 or float64")
+
+
+def upload(n_rows, n_cols, indptr, indices, values, *, device=None, non_blocking=True):
+    """DeviceCsr from host arrays (numpy or CPU torch tensors; pinned tensors
+    make the H2D copies asynchronous).  ``values``' dtype (float32/float64)
+    is the compute dtype."""
+    import torch
+
+    def dev_tensor(x, dt):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+        if t.dtype != dt:
+            t = t.to(dt)
+        return t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()),
+                    non_blocking=non_blocking and t.is_pinned())
+
+    vt = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values))
+    if vt.dtype not in (torch.float32, torch.float64):
+        vt = vt.to(torch.float64)
+    d = DeviceCsr(int(n_rows), int(n_cols), dev_tensor(indptr, torch.int64), dev_tensor(indices, torch.int32),
+                  dev_tensor(vt, vt.dtype))
+    host_ptr = indptr.numpy() if isinstance(indptr, torch.Tensor) else np.asarray(indptr)
+    d._host_degrees = np.diff(host_ptr.astype(np.int64))
+    return d
