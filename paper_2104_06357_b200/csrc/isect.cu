@@ -132,7 +132,11 @@ struct IsectArgs {
   int tile;
   int64_t n_tiles, n, n_cols;
   const T* sa0; const T* sa1; const T* sb0; const T* sb1;
-  const int32_t* order;
+  // work plan (plan_kernel): items are (query, tile range) pairs
+  const int32_t* order;     // order[p] = query at plan position p (longest first)
+  const int32_t* tpi;       // tiles per item of position p
+  const int64_t* item_off;  // items of position p: [item_off[p], item_off[p+1])
+  const int32_t* item_pos;  // item -> plan position
   unsigned int* counter;
   int metric, strict;
   T k, p;
@@ -140,12 +144,12 @@ struct IsectArgs {
   int64_t ldo;
   uint32_t* flags;
   int topk;
-  int64_t index_base;
-  T* out_d;
-  int64_t* out_i;
+  T* cand_d;                // kNN: per-item candidate lists [items][topk]
+  int64_t* cand_i;
 };
 
-constexpr int ISECT_U = 8;  // columns whose first postings are in flight at once
+// columns whose first 32 postings are loaded before any is applied
+template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
 
 template <typename T, int CK>
 __device__ __forceinline__ T fused_value(const IsectArgs<T>& a, T acc, T cnt, T ra0, T ra1, T rb0, T rb1,
@@ -170,136 +174,185 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool KL = CK == C_KL;
   constexpr unsigned FULL = 0xffffffffu;
+  constexpr int U = IsectU<T>::value;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int TJ = a.tile;
   T* acc = reinterpret_cast<T*>(smem) + size_t(warp) * TJ * (KL ? 2 : 1);
   T* cnt = acc + TJ;
   const T p = a.p;
+  const int64_t total_items = a.item_off[a.m];
   uint32_t flags = 0;
 
+  for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
+    acc[q] = T(0);
+    if constexpr (KL) cnt[q] = T(0);
+  }
+  __syncwarp();
+
   while (true) {
-    unsigned qi = 0;
-    if (lane == 0) qi = atomicAdd(a.counter, 1u);
-    qi = __shfl_sync(FULL, qi, 0);
-    if (int64_t(qi) >= a.m) break;
-    const int64_t i = a.order ? int64_t(a.order[qi]) : int64_t(qi);
+    unsigned item = 0;
+    if (lane == 0) item = atomicAdd(a.counter, 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (int64_t(item) >= total_items) break;
+    const int pos = a.item_pos[item];
+    const int64_t i = a.order[pos];
+    const int64_t tpi = a.tpi[pos];
+    const int64_t t0 = (int64_t(item) - a.item_off[pos]) * tpi;
+    const int64_t t1 = tmin<int64_t>(a.n_tiles, t0 + tpi);
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
     const T ra0 = a.sa0 ? a.sa0[i] : T(0);
     const T ra1 = a.sa1 ? a.sa1[i] : T(0);
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
     if constexpr (KPL > 0) top.init();
 
-    for (int64_t t = 0; t < a.n_tiles; ++t) {
+    for (int64_t t = t0; t < t1; ++t) {
       const int64_t j0 = t * TJ;
       const int nt = int(tmin<int64_t>(TJ, a.n - j0));
-      for (int q = lane; q < nt; q += 32) {
-        acc[q] = T(0);
-        if constexpr (KL) cnt[q] = T(0);
-      }
-      __syncwarp();
       const uint32_t* cp = a.colptr + t * a.n_cols;
+      // software pipeline: (column, value, posting range) of the next 32 columns
+      int64_t e = abeg + lane;
+      bool valid = e < aend;
+      int32_t c = valid ? a.a_idx[e] : 0;
+      T av = valid ? a.a_val[e] : T(0);
+      uint32_t pb = valid ? cp[c] : 0u;
+      uint32_t pe = valid ? cp[c + 1] : 0u;
       for (int64_t base = abeg; base < aend; base += 32) {
-        const int64_t e = base + lane;
-        const bool valid = e < aend;
-        const int32_t c = valid ? a.a_idx[e] : 0;
-        const T av = valid ? a.a_val[e] : T(0);
-        const uint32_t pb = valid ? cp[c] : 0u;
-        const uint32_t pe = valid ? cp[c + 1] : 0u;
         const int ncol = int(tmin<int64_t>(32, aend - base));
-        for (int q0 = 0; q0 < ncol; q0 += ISECT_U) {
-          uint32_t b0[ISECT_U], b1[ISECT_U];
-          T x[ISECT_U], y[ISECT_U];
-          int jl[ISECT_U];
+        const uint32_t cur_pb = pb, cur_pe = pe;
+        const T cur_av = av;
+        // next batch's columns (independent of this batch's postings)
+        e = base + 32 + lane;
+        valid = e < aend;
+        c = valid ? a.a_idx[e] : 0;
+        av = valid ? a.a_val[e] : T(0);
+        for (int q0 = 0; q0 < ncol; q0 += U) {
+          int jl[U];
+          T y[U];
 #pragma unroll
-          for (int u = 0; u < ISECT_U; ++u) {
-            const int q = (q0 + u) & 31;
-            b0[u] = __shfl_sync(FULL, pb, q);
-            b1[u] = __shfl_sync(FULL, pe, q);
-            x[u] = __shfl_sync(FULL, av, q);
-            if (q0 + u >= ncol) b1[u] = b0[u];
-            const uint32_t pp = b0[u] + lane;
-            jl[u] = 0;
+          for (int u = 0; u < U; ++u) {
+            const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
+            const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
+            const uint32_t pp = b0 + lane;
+            jl[u] = -1;
             y[u] = T(0);
-            if (pp < b1[u]) {
+            if (q0 + u < ncol && pp < b1) {
               jl[u] = a.pj[pp];
               y[u] = a.pv[pp];
             }
           }
+          if (q0 + U >= ncol) {  // last group of this batch: start the next batch's colptr loads
+            pb = valid ? cp[c] : 0u;
+            pe = valid ? cp[c + 1] : 0u;
+          }
 #pragma unroll
-          for (int u = 0; u < ISECT_U; ++u) {
-            const uint32_t pp = b0[u] + lane;
-            if (pp < b1[u]) {
-              acc[jl[u]] = add_rn(acc[jl[u]], contrib<CK, T>(x[u], y[u], p));
-              if constexpr (KL) cnt[jl[u]] = add_rn(cnt[jl[u]], T(1));
-              for (uint32_t p2 = pp + 32; p2 < b1[u]; p2 += 32) {
+          for (int u = 0; u < U; ++u) {
+            if (q0 + u < ncol) {
+              const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
+              if (jl[u] >= 0) {
+                acc[jl[u]] = add_rn(acc[jl[u]], contrib<CK, T>(x, y[u], p));
+                if constexpr (KL) cnt[jl[u]] = add_rn(cnt[jl[u]], T(1));
+              }
+              const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
+              const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
+              for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {  // columns with > 32 postings in this tile
                 const int j2 = a.pj[p2];
-                acc[j2] = add_rn(acc[j2], contrib<CK, T>(x[u], a.pv[p2], p));
+                acc[j2] = add_rn(acc[j2], contrib<CK, T>(x, a.pv[p2], p));
                 if constexpr (KL) cnt[j2] = add_rn(cnt[j2], T(1));
               }
+              __syncwarp();
             }
-            __syncwarp();
           }
         }
       }
-      // epilogue over the tile's cells
+      // epilogue over the tile's cells; the accumulator is re-zeroed as it is read
       for (int q = 0; q < nt; q += 32) {
         const int l = q + lane;
-        const bool valid = l < nt;
+        const bool ok = l < nt;
         const int64_t j = j0 + l;
         T d = T(0);
-        if (valid) {
+        if (ok) {
+          const T v = acc[l];
+          acc[l] = T(0);
+          T cv = T(0);
+          if constexpr (KL) { cv = cnt[l]; cnt[l] = T(0); }
           const T rb0 = a.sb0 ? a.sb0[j] : T(0);
           const T rb1 = a.sb1 ? a.sb1[j] : T(0);
-          d = fused_value<T, CK>(a, acc[l], KL ? cnt[l] : T(0), ra0, ra1, rb0, rb1, flags);
+          d = fused_value<T, CK>(a, v, cv, ra0, ra1, rb0, rb1, flags);
         }
         if constexpr (KPL > 0) {
-          top.offer(valid, d, j, a.topk);
+          top.offer(ok, d, j, a.topk);
         } else {
-          if (valid) a.out[i * a.ldo + j] = d;
+          if (ok) a.out[i * a.ldo + j] = d;
         }
       }
       __syncwarp();
     }
-    if constexpr (KPL > 0) top.store(a.topk, a.out_d + i * a.topk, a.out_i + i * a.topk, a.index_base);
+    if constexpr (KPL > 0)
+      top.store(a.topk, a.cand_d + int64_t(item) * a.topk, a.cand_i + int64_t(item) * a.topk, 0);
   }
   flags = __reduce_or_sync(FULL, flags);
   if (flags && lane == 0) atomicOr(a.flags, flags);
 }
 
+// kNN: merge the per-item candidate lists of each query into its top-k.
+template <typename T, int KPL>
+__global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __restrict__ ci,
+                                   const int32_t* __restrict__ order, const int64_t* __restrict__ item_off,
+                                   int64_t m, int k, int64_t base, T* __restrict__ od, int64_t* __restrict__ oi) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t p = warp; p < m; p += nw) {
+    WarpTopK<T, KPL> top;
+    top.init();
+    for (int64_t it = item_off[p]; it < item_off[p + 1]; ++it)
+      for (int q = 0; q < k; q += 32) {
+        const int j = q + int(lane_id());
+        const bool ok = j < k;
+        top.offer(ok, ok ? cd[it * k + j] : T(0), ok ? ci[it * k + j] : 0, k);
+      }
+    const int64_t i = order[p];
+    top.store(k, od + i * k, oi + i * k, base);
+  }
+}
+
 template <typename T, int CK, int KPL>
-static int launch_isect(IsectArgs<T>& args, cudaStream_t st) {
-  const int64_t optin = smem_optin_bytes() - static_smem((const void*)isect_kernel<T, CK, KPL>);
+static int launch_isect(IsectArgs<T>& args, int W, cudaStream_t st) {
   const int64_t per_warp = int64_t(args.tile) * sizeof(T) * (CK == C_KL ? 2 : 1);
-  int W = int(std::min<int64_t>(16, (optin - 1024) / per_warp));
-  if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const size_t smem = size_t(W) * per_warp;
   SD_TRY(prepare_smem(isect_kernel<T, CK, KPL>, smem, "isect_kernel"));
   int per_sm = 0;
   SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, isect_kernel<T, CK, KPL>, W * 32, smem));
   per_sm = std::max(1, per_sm);
-  const int64_t warps_needed = args.m;
-  int64_t blocks = std::min<int64_t>(int64_t(num_sms()) * per_sm, (warps_needed + W - 1) / W);
-  blocks = std::max<int64_t>(1, blocks);
+  const int64_t blocks = std::max<int64_t>(1, int64_t(num_sms()) * per_sm);
   isect_kernel<T, CK, KPL><<<unsigned(blocks), W * 32, smem, st>>>(args);
   SD_LAUNCH_CHECK();
   return SD_OK;
 }
 
-// Query schedule: rows ordered by descending floor(log2(degree)) so the
-// dynamic queue hands out the longest rows first (LPT).  One CTA: bucket
-// histogram, scan, scatter — no library sort in the hot path.
-__global__ void __launch_bounds__(1024) degree_order_kernel(const int64_t* __restrict__ ptr, int64_t m,
-                                                            int32_t* __restrict__ order) {
+// Work plan (one CTA, no library sort): queries ordered by descending
+// floor(log2(degree)) (LPT), each split into items of `tpi` consecutive tiles
+// so that every item costs about total/(8·warps) — a power-law query of
+// degree 25k is spread over up to n_tiles warps instead of serialising on one.
+__global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ ptr, int64_t m, int64_t n_tiles,
+                                                    int64_t warps, int64_t epi_cost, int32_t* __restrict__ order,
+                                                    int32_t* __restrict__ tpi, int64_t* __restrict__ item_off,
+                                                    int32_t* __restrict__ item_pos) {
   __shared__ unsigned int hist[64];
   __shared__ unsigned int base[64];
+  __shared__ unsigned long long total;
+  __shared__ int64_t part[1024];
   if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) total = 0;
   __syncthreads();
+  unsigned long long local = 0;
   for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
     const int64_t d = ptr[r + 1] - ptr[r];
-    const int b = d > 0 ? 63 - __clzll(d) : 0;   // floor(log2 d)
-    atomicAdd(&hist[63 - b], 1u);                // descending degree
+    const int b = d > 0 ? 63 - __clzll(d) : 0;
+    atomicAdd(&hist[63 - b], 1u);
+    local += (unsigned long long)(d + epi_cost);
   }
+  atomicAdd(&total, local);
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int acc = 0;
@@ -311,13 +364,34 @@ __global__ void __launch_bounds__(1024) degree_order_kernel(const int64_t* __res
     const int b = d > 0 ? 63 - __clzll(d) : 0;
     order[atomicAdd(&base[63 - b], 1u)] = int32_t(r);
   }
-}
-
-static int degree_order(const sd_csr* a, cudaStream_t st, Scratch& order_buf) {
-  SD_TRY(order_buf.alloc(sizeof(int32_t) * std::max<int64_t>(1, a->n_rows), st));
-  degree_order_kernel<<<1, 1024, 0, st>>>(a->indptr, a->n_rows, order_buf.as<int32_t>());
-  SD_LAUNCH_CHECK();
-  return SD_OK;
+  __syncthreads();
+  const int64_t target = tmax<int64_t>(1, int64_t(total) * n_tiles / tmax<int64_t>(1, warps * 8));
+  // contiguous chunk per thread: items per position, then a block scan
+  const int64_t chunk = (m + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = tmin<int64_t>(m, int64_t(threadIdx.x) * chunk), hi = tmin<int64_t>(m, lo + chunk);
+  int64_t sum = 0;
+  for (int64_t q = lo; q < hi; ++q) {
+    const int64_t r = order[q];
+    const int64_t cost = ptr[r + 1] - ptr[r] + epi_cost;
+    const int64_t t = tmin<int64_t>(n_tiles, tmax<int64_t>(1, target / cost));
+    tpi[q] = int32_t(t);
+    sum += (n_tiles + t - 1) / t;
+  }
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int t = 0; t < int(blockDim.x); ++t) { const int64_t v = part[t]; part[t] = acc; acc += v; }
+    item_off[m] = acc;
+  }
+  __syncthreads();
+  int64_t off = part[threadIdx.x];
+  for (int64_t q = lo; q < hi; ++q) {
+    item_off[q] = off;
+    const int64_t cnt = (n_tiles + tpi[q] - 1) / tpi[q];
+    for (int64_t it = 0; it < cnt; ++it) item_pos[off + it] = int32_t(q);
+    off += cnt;
+  }
 }
 
 // Per-row statistics of both sides for the fused epilogue (norms for the
@@ -346,31 +420,60 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     set_error("index does not match B / dtype");
     return SD_E_INVALID;
   }
-  if (a->n_rows == 0 || b->n_rows == 0) return SD_OK;
-  Scratch order, counter;
-  SD_TRY(degree_order(a, st, order));
+  const int64_t m = a->n_rows;
+  if (m == 0 || b->n_rows == 0) return SD_OK;
+  if (m >= (int64_t(1) << 31)) { set_error("too many query rows"); return SD_E_INVALID; }
+  const size_t es = dtype == SD_F64 ? 8 : 4;
+  const int64_t per_warp = int64_t(ix->tile) * int64_t(es) * (ck == C_KL ? 2 : 1);
+  const int W = int(std::min<int64_t>(16, (smem_optin_bytes() - 2048) / per_warp));
+  if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
+  const int64_t warps = int64_t(num_sms()) * W;
+  const int64_t max_items = m * ix->n_tiles;
+  Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
+  SD_TRY(order.alloc(sizeof(int32_t) * m, st));
+  SD_TRY(tpi.alloc(sizeof(int32_t) * m, st));
+  SD_TRY(item_off.alloc(sizeof(int64_t) * (m + 1), st));
+  SD_TRY(item_pos.alloc(sizeof(int32_t) * max_items, st));
   SD_TRY(counter.alloc(sizeof(unsigned int), st));
   SD_CUDA_TRY(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int), st));
+  plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, warps, ix->tile / 16, order.as<int32_t>(),
+                                  tpi.as<int32_t>(), item_off.as<int64_t>(), item_pos.as<int32_t>());
+  SD_LAUNCH_CHECK();
+  if (topk > 0) {
+    SD_TRY(cand_d.alloc(es * size_t(max_items) * topk, st));
+    SD_TRY(cand_i.alloc(sizeof(int64_t) * size_t(max_items) * topk, st));
+  }
   return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
     IsectArgs<T> args;
     args.a_ptr = a->indptr; args.a_idx = a->indices; args.a_val = static_cast<const T*>(a->values);
-    args.m = a->n_rows;
+    args.m = m;
     args.colptr = ix->colptr; args.pj = ix->post_j; args.pv = static_cast<const T*>(ix->post_v);
     args.tile = ix->tile; args.n_tiles = ix->n_tiles; args.n = ix->n_rows; args.n_cols = ix->n_cols;
     args.sa0 = static_cast<const T*>(sa.s[0]); args.sa1 = static_cast<const T*>(sa.s[1]);
     args.sb0 = static_cast<const T*>(sb.s[0]); args.sb1 = static_cast<const T*>(sb.s[1]);
-    args.order = order.as<int32_t>();
+    args.order = order.as<int32_t>(); args.tpi = tpi.as<int32_t>();
+    args.item_off = item_off.as<int64_t>(); args.item_pos = item_pos.as<int32_t>();
     args.counter = counter.as<unsigned int>();
     args.metric = md->metric; args.strict = md->strict;
     args.k = T(a->n_cols); args.p = T(md->p);
     args.out = static_cast<T*>(out); args.ldo = ldo; args.flags = flags;
-    args.topk = topk; args.index_base = index_base;
-    args.out_d = static_cast<T*>(out_d); args.out_i = out_i;
+    args.topk = topk;
+    args.cand_d = cand_d.as<T>(); args.cand_i = cand_i.as<int64_t>();
     auto go = [&](auto ck_tag) -> int {
       constexpr int CK = decltype(ck_tag)::value;
-      if (topk <= 0) return launch_isect<T, CK, 0>(args, st);
-      if (topk <= 32) return launch_isect<T, CK, 1>(args, st);
-      return launch_isect<T, CK, 4>(args, st);
+      if (topk <= 0) return launch_isect<T, CK, 0>(args, W, st);
+      const int blocks = int(std::min<int64_t>((m * 32 + 255) / 256, int64_t(num_sms()) * 16));
+      if (topk <= 32) {
+        SD_TRY((launch_isect<T, CK, 1>(args, W, st)));
+        merge_items_kernel<T, 1><<<blocks, 256, 0, st>>>(args.cand_d, args.cand_i, args.order, args.item_off, m,
+                                                        topk, index_base, static_cast<T*>(out_d), out_i);
+      } else {
+        SD_TRY((launch_isect<T, CK, 4>(args, W, st)));
+        merge_items_kernel<T, 4><<<blocks, 256, 0, st>>>(args.cand_d, args.cand_i, args.order, args.item_off, m,
+                                                        topk, index_base, static_cast<T*>(out_d), out_i);
+      }
+      SD_LAUNCH_CHECK();
+      return SD_OK;
     };
     switch (ck) {
       case C_MUL: return go(std::integral_constant<int, C_MUL>());
