@@ -24,6 +24,7 @@
 #include "metric.cuh"
 #include "prep.cuh"
 #include "topk.cuh"
+#include "isect_kernel.cuh"
 
 struct sd_index {
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
@@ -115,218 +116,6 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
     if (rc != SD_OK) return fail(rc);
   }
   *out = ix;
-  return SD_OK;
-}
-
-// ---------------------------------------------------------------- kernel
-
-template <typename T>
-struct IsectArgs {
-  const int64_t* a_ptr;
-  const int32_t* a_idx;
-  const T* a_val;
-  int64_t m;
-  const uint32_t* colptr;
-  const uint16_t* pj;
-  const T* pv;
-  int tile;
-  int64_t n_tiles, n, n_cols;
-  const T* sa0; const T* sa1; const T* sb0; const T* sb1;
-  // work plan (plan_kernel): items are (query, tile range) pairs
-  const int32_t* order;     // order[p] = query at plan position p (longest first)
-  const int32_t* tpi;       // tiles per item of position p
-  const int64_t* item_off;  // items of position p: [item_off[p], item_off[p+1])
-  const int32_t* item_pos;  // item -> plan position
-  unsigned int* counter;
-  int metric, strict;
-  T k, p;
-  T* out;
-  int64_t ldo;
-  uint32_t* flags;
-  int topk;
-  T* cand_d;                // kNN: per-item candidate lists [items][topk]
-  int64_t* cand_i;
-};
-
-// columns whose first 32 postings are loaded before any is applied
-template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
-
-template <typename T, int CK>
-__device__ __forceinline__ T fused_value(const IsectArgs<T>& a, T acc, T cnt, T ra0, T ra1, T rb0, T rb1,
-                                         uint32_t& flags) {
-  if constexpr (CK == C_KL) {
-    if (cnt != ra0) {  // some column of A_i is absent from B_j (metrics.py:352-366)
-      if (a.strict) flags |= SD_FLAG_KL_UNCOVERED;
-      return Num<T>::big();
-    }
-    return acc;
-  } else if constexpr (CK == C_MUL) {
-    return expand_cell<T>(a.metric, acc, ra0, ra1, rb0, rb1, a.k, a.p, flags);
-  } else {
-    T x = add_rn(add_rn(ra0, rb0), acc);
-    x = x < T(0) ? T(0) : x;  // cancellation residue of the union decomposition
-    return expand_cell<T>(a.metric, x, T(0), T(0), T(0), T(0), a.k, a.p, flags);
-  }
-}
-
-template <typename T, int CK, int KPL>
-__global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr bool KL = CK == C_KL;
-  constexpr unsigned FULL = 0xffffffffu;
-  constexpr int U = IsectU<T>::value;
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int TJ = a.tile;
-  T* acc = reinterpret_cast<T*>(smem) + size_t(warp) * TJ * (KL ? 2 : 1);
-  T* cnt = acc + TJ;
-  const T p = a.p;
-  const int64_t total_items = a.item_off[a.m];
-  uint32_t flags = 0;
-
-  for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
-    acc[q] = T(0);
-    if constexpr (KL) cnt[q] = T(0);
-  }
-  __syncwarp();
-
-  while (true) {
-    unsigned item = 0;
-    if (lane == 0) item = atomicAdd(a.counter, 1u);
-    item = __shfl_sync(FULL, item, 0);
-    if (int64_t(item) >= total_items) break;
-    const int pos = a.item_pos[item];
-    const int64_t i = a.order[pos];
-    const int64_t tpi = a.tpi[pos];
-    const int64_t t0 = (int64_t(item) - a.item_off[pos]) * tpi;
-    const int64_t t1 = tmin<int64_t>(a.n_tiles, t0 + tpi);
-    const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
-    const T ra0 = a.sa0 ? a.sa0[i] : T(0);
-    const T ra1 = a.sa1 ? a.sa1[i] : T(0);
-    WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
-    if constexpr (KPL > 0) top.init();
-
-    for (int64_t t = t0; t < t1; ++t) {
-      const int64_t j0 = t * TJ;
-      const int nt = int(tmin<int64_t>(TJ, a.n - j0));
-      const uint32_t* cp = a.colptr + t * a.n_cols;
-      // software pipeline: (column, value, posting range) of the next 32 columns
-      int64_t e = abeg + lane;
-      bool valid = e < aend;
-      int32_t c = valid ? a.a_idx[e] : 0;
-      T av = valid ? a.a_val[e] : T(0);
-      uint32_t pb = valid ? cp[c] : 0u;
-      uint32_t pe = valid ? cp[c + 1] : 0u;
-      for (int64_t base = abeg; base < aend; base += 32) {
-        const int ncol = int(tmin<int64_t>(32, aend - base));
-        const uint32_t cur_pb = pb, cur_pe = pe;
-        const T cur_av = av;
-        // next batch's columns (independent of this batch's postings)
-        e = base + 32 + lane;
-        valid = e < aend;
-        c = valid ? a.a_idx[e] : 0;
-        av = valid ? a.a_val[e] : T(0);
-        for (int q0 = 0; q0 < ncol; q0 += U) {
-          int jl[U];
-          T y[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
-            const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
-            const uint32_t pp = b0 + lane;
-            jl[u] = -1;
-            y[u] = T(0);
-            if (q0 + u < ncol && pp < b1) {
-              jl[u] = a.pj[pp];
-              y[u] = a.pv[pp];
-            }
-          }
-          if (q0 + U >= ncol) {  // last group of this batch: start the next batch's colptr loads
-            pb = valid ? cp[c] : 0u;
-            pe = valid ? cp[c + 1] : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (q0 + u < ncol) {
-              const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
-              if (jl[u] >= 0) {
-                acc[jl[u]] = add_rn(acc[jl[u]], contrib<CK, T>(x, y[u], p));
-                if constexpr (KL) cnt[jl[u]] = add_rn(cnt[jl[u]], T(1));
-              }
-              const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
-              const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
-              for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {  // columns with > 32 postings in this tile
-                const int j2 = a.pj[p2];
-                acc[j2] = add_rn(acc[j2], contrib<CK, T>(x, a.pv[p2], p));
-                if constexpr (KL) cnt[j2] = add_rn(cnt[j2], T(1));
-              }
-              __syncwarp();
-            }
-          }
-        }
-      }
-      // epilogue over the tile's cells; the accumulator is re-zeroed as it is read
-      for (int q = 0; q < nt; q += 32) {
-        const int l = q + lane;
-        const bool ok = l < nt;
-        const int64_t j = j0 + l;
-        T d = T(0);
-        if (ok) {
-          const T v = acc[l];
-          acc[l] = T(0);
-          T cv = T(0);
-          if constexpr (KL) { cv = cnt[l]; cnt[l] = T(0); }
-          const T rb0 = a.sb0 ? a.sb0[j] : T(0);
-          const T rb1 = a.sb1 ? a.sb1[j] : T(0);
-          d = fused_value<T, CK>(a, v, cv, ra0, ra1, rb0, rb1, flags);
-        }
-        if constexpr (KPL > 0) {
-          top.offer(ok, d, j, a.topk);
-        } else {
-          if (ok) a.out[i * a.ldo + j] = d;
-        }
-      }
-      __syncwarp();
-    }
-    if constexpr (KPL > 0)
-      top.store(a.topk, a.cand_d + int64_t(item) * a.topk, a.cand_i + int64_t(item) * a.topk, 0);
-  }
-  flags = __reduce_or_sync(FULL, flags);
-  if (flags && lane == 0) atomicOr(a.flags, flags);
-}
-
-// kNN: merge the per-item candidate lists of each query into its top-k.
-template <typename T, int KPL>
-__global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __restrict__ ci,
-                                   const int32_t* __restrict__ order, const int64_t* __restrict__ item_off,
-                                   int64_t m, int k, int64_t base, T* __restrict__ od, int64_t* __restrict__ oi) {
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t p = warp; p < m; p += nw) {
-    WarpTopK<T, KPL> top;
-    top.init();
-    for (int64_t it = item_off[p]; it < item_off[p + 1]; ++it)
-      for (int q = 0; q < k; q += 32) {
-        const int j = q + int(lane_id());
-        const bool ok = j < k;
-        top.offer(ok, ok ? cd[it * k + j] : T(0), ok ? ci[it * k + j] : 0, k);
-      }
-    const int64_t i = order[p];
-    top.store(k, od + i * k, oi + i * k, base);
-  }
-}
-
-template <typename T, int CK, int KPL>
-static int launch_isect(IsectArgs<T>& args, int W, cudaStream_t st) {
-  const int64_t per_warp = int64_t(args.tile) * sizeof(T) * (CK == C_KL ? 2 : 1);
-  const size_t smem = size_t(W) * per_warp;
-  SD_TRY(prepare_smem(isect_kernel<T, CK, KPL>, smem, "isect_kernel"));
-  int per_sm = 0;
-  SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, isect_kernel<T, CK, KPL>, W * 32, smem));
-  per_sm = std::max(1, per_sm);
-  const int64_t blocks = std::max<int64_t>(1, int64_t(num_sms()) * per_sm);
-  isect_kernel<T, CK, KPL><<<unsigned(blocks), W * 32, smem, st>>>(args);
-  SD_LAUNCH_CHECK();
   return SD_OK;
 }
 
@@ -454,36 +243,14 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.order = order.as<int32_t>(); args.tpi = tpi.as<int32_t>();
     args.item_off = item_off.as<int64_t>(); args.item_pos = item_pos.as<int32_t>();
     args.counter = counter.as<unsigned int>();
-    args.metric = md->metric; args.strict = md->strict;
+    args.strict = md->strict;
     args.k = T(a->n_cols); args.p = T(md->p);
     args.out = static_cast<T*>(out); args.ldo = ldo; args.flags = flags;
     args.topk = topk;
     args.cand_d = cand_d.as<T>(); args.cand_i = cand_i.as<int64_t>();
-    auto go = [&](auto ck_tag) -> int {
-      constexpr int CK = decltype(ck_tag)::value;
-      if (topk <= 0) return launch_isect<T, CK, 0>(args, W, st);
-      const int blocks = int(std::min<int64_t>((m * 32 + 255) / 256, int64_t(num_sms()) * 16));
-      if (topk <= 32) {
-        SD_TRY((launch_isect<T, CK, 1>(args, W, st)));
-        merge_items_kernel<T, 1><<<blocks, 256, 0, st>>>(args.cand_d, args.cand_i, args.order, args.item_off, m,
-                                                        topk, index_base, static_cast<T*>(out_d), out_i);
-      } else {
-        SD_TRY((launch_isect<T, CK, 4>(args, W, st)));
-        merge_items_kernel<T, 4><<<blocks, 256, 0, st>>>(args.cand_d, args.cand_i, args.order, args.item_off, m,
-                                                        topk, index_base, static_cast<T*>(out_d), out_i);
-      }
-      SD_LAUNCH_CHECK();
-      return SD_OK;
-    };
-    switch (ck) {
-      case C_MUL: return go(std::integral_constant<int, C_MUL>());
-      case C_KL: return go(std::integral_constant<int, C_KL>());
-      case C_ABS: return go(std::integral_constant<int, C_ABS>());
-      case C_ABSPOW: return go(std::integral_constant<int, C_ABSPOW>());
-      case C_CANBERRA: return go(std::integral_constant<int, C_CANBERRA>());
-      case C_MISMATCH: return go(std::integral_constant<int, C_MISMATCH>());
-      default: return go(std::integral_constant<int, C_JS>());
-    }
+    SD_TRY(isect_launch(args, md->metric, W, st));
+    if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
+    return SD_OK;
   });
 }
 

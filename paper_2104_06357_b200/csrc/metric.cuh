@@ -39,58 +39,68 @@ __device__ __forceinline__ T root_p(T x, T p) {
 //   correlation: s0 = signed sum, s1 = l2sq     cosine: s0 = l2
 //   dice, jaccard: s0 = l0                        euclidean: s0 = l2sq
 //   kl (A side): s0 = l0 (coverage test)          NAMM (fused path): s0 = one-sided sum
+template <int M, typename T>
+__device__ __forceinline__ T expand_cell_t(T d, T a0, T a1, T b0, T b1, T k, T p, uint32_t& flags) {
+  if constexpr (M == SD_M_CORRELATION) {  // metrics.py:121-132
+    T fa = clamp_radicand(sub_rn(mul_rn(k, a1), mul_rn(a0, a0)), mul_rn(k, a1), flags);
+    T fb = clamp_radicand(sub_rn(mul_rn(k, b1), mul_rn(b0, b0)), mul_rn(k, b1), flags);
+    T denom = sqrt_rn(mul_rn(fa, fb));
+    T num = sub_rn(mul_rn(k, d), mul_rn(a0, b0));
+    if (denom > T(0)) return sub_rn(T(1), div_rn(num, denom));
+    return (a1 == T(0) && b1 == T(0)) ? T(0) : T(1);
+  } else if constexpr (M == SD_M_COSINE) {  // metrics.py:112-118
+    T denom = mul_rn(a0, b0);
+    if (denom > T(0)) return sub_rn(T(1), div_rn(d, denom));
+    return (a0 == T(0) && b0 == T(0)) ? T(0) : T(1);
+  } else if constexpr (M == SD_M_DICE) {  // metrics.py:135-140
+    T denom = add_rn(a0, b0);
+    return denom > T(0) ? sub_rn(T(1), div_rn(mul_rn(T(2), d), denom)) : T(0);
+  } else if constexpr (M == SD_M_DOT || M == SD_M_KL) {  // metrics.py:102-103
+    return d;
+  } else if constexpr (M == SD_M_EUCLIDEAN) {  // metrics.py:106-109 + _sqrt_post 162-163
+    T x = add_rn(sub_rn(a0, mul_rn(T(2), d)), b0);
+    return sqrt_rn(clamp_radicand(x, add_rn(a0, b0), flags));
+  } else if constexpr (M == SD_M_HELLINGER) {  // metrics.py:158-159
+    return sub_rn(T(1), sqrt_rn(clamp_radicand(d, T(1), flags)));
+  } else if constexpr (M == SD_M_JACCARD) {  // metrics.py:143-149
+    T denom = sub_rn(add_rn(a0, b0), d);
+    if (denom > T(0)) return sub_rn(T(1), div_rn(d, denom));
+    return (a0 == T(0) && b0 == T(0)) ? T(0) : T(1);
+  } else if constexpr (M == SD_M_RUSSELRAO) {  // metrics.py:152-155
+    return k == T(0) ? T(0) : div_rn(sub_rn(k, d), k);
+  } else if constexpr (M == SD_M_HAMMING) {  // _mean_post, metrics.py:175-176
+    return k != T(0) ? div_rn(d, k) : T(0);
+  } else if constexpr (M == SD_M_JENSENSHANNON) {  // _js_post, metrics.py:179-180
+    return sqrt_rn(div_rn(clamp_radicand(d, T(0), flags), T(2)));
+  } else if constexpr (M == SD_M_MINKOWSKI) {  // _root_post, metrics.py:166-172
+    return root_p(d, p);
+  } else {  // canberra, chebyshev, manhattan: identity
+    return d;
+  }
+}
+
+// runtime-dispatched form (element-wise expansion kernel, expansion_apply)
 template <typename T>
-__device__ __forceinline__ T expand_cell(int metric, T d, T a0, T a1, T b0, T b1, T k, T p,
-                                         uint32_t& flags) {
+__device__ __forceinline__ T expand_cell(int metric, T d, T a0, T a1, T b0, T b1, T k, T p, uint32_t& flags) {
   switch (metric) {
-    case SD_M_CORRELATION: {  // metrics.py:121-132
-      T fa = clamp_radicand(sub_rn(mul_rn(k, a1), mul_rn(a0, a0)), mul_rn(k, a1), flags);
-      T fb = clamp_radicand(sub_rn(mul_rn(k, b1), mul_rn(b0, b0)), mul_rn(k, b1), flags);
-      T denom = sqrt_rn(mul_rn(fa, fb));
-      T num = sub_rn(mul_rn(k, d), mul_rn(a0, b0));
-      if (denom > T(0)) return sub_rn(T(1), div_rn(num, denom));
-      return (a1 == T(0) && b1 == T(0)) ? T(0) : T(1);
-    }
-    case SD_M_COSINE: {  // metrics.py:112-118
-      T denom = mul_rn(a0, b0);
-      if (denom > T(0)) return sub_rn(T(1), div_rn(d, denom));
-      return (a0 == T(0) && b0 == T(0)) ? T(0) : T(1);
-    }
-    case SD_M_DICE: {  // metrics.py:135-140
-      T denom = add_rn(a0, b0);
-      return denom > T(0) ? sub_rn(T(1), div_rn(mul_rn(T(2), d), denom)) : T(0);
-    }
-    case SD_M_DOT:  // metrics.py:102-103
-    case SD_M_KL:
-      return d;
-    case SD_M_EUCLIDEAN: {  // metrics.py:106-109 + _sqrt_post 162-163
-      T x = add_rn(sub_rn(a0, mul_rn(T(2), d)), b0);
-      return sqrt_rn(clamp_radicand(x, add_rn(a0, b0), flags));
-    }
-    case SD_M_HELLINGER:  // metrics.py:158-159
-      return sub_rn(T(1), sqrt_rn(clamp_radicand(d, T(1), flags)));
-    case SD_M_JACCARD: {  // metrics.py:143-149
-      T denom = sub_rn(add_rn(a0, b0), d);
-      if (denom > T(0)) return sub_rn(T(1), div_rn(d, denom));
-      return (a0 == T(0) && b0 == T(0)) ? T(0) : T(1);
-    }
-    case SD_M_RUSSELRAO:  // metrics.py:152-155
-      return k == T(0) ? T(0) : div_rn(sub_rn(k, d), k);
-    case SD_M_HAMMING:  // _mean_post, metrics.py:175-176
-      return k != T(0) ? div_rn(d, k) : T(0);
-    case SD_M_JENSENSHANNON:  // _js_post, metrics.py:179-180
-      return sqrt_rn(div_rn(clamp_radicand(d, T(0), flags), T(2)));
-    case SD_M_MINKOWSKI:  // _root_post, metrics.py:166-172
-      return root_p(d, p);
-    default:  // canberra, chebyshev, manhattan: identity
-      return d;
+    case SD_M_CORRELATION: return expand_cell_t<SD_M_CORRELATION, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_COSINE: return expand_cell_t<SD_M_COSINE, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_DICE: return expand_cell_t<SD_M_DICE, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_EUCLIDEAN: return expand_cell_t<SD_M_EUCLIDEAN, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_HELLINGER: return expand_cell_t<SD_M_HELLINGER, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_JACCARD: return expand_cell_t<SD_M_JACCARD, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_RUSSELRAO: return expand_cell_t<SD_M_RUSSELRAO, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_HAMMING: return expand_cell_t<SD_M_HAMMING, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_JENSENSHANNON: return expand_cell_t<SD_M_JENSENSHANNON, T>(d, a0, a1, b0, b1, k, p, flags);
+    case SD_M_MINKOWSKI: return expand_cell_t<SD_M_MINKOWSKI, T>(d, a0, a1, b0, b1, k, p, flags);
+    default: return d;
   }
 }
 
 // ---- contributions of one intersecting column for the fused path
 enum ContribKind { C_MUL = 0, C_KL = 1, C_ABS = 2, C_ABSPOW = 3, C_CANBERRA = 4, C_MISMATCH = 5, C_JS = 6 };
 
-__host__ __device__ inline int metric_contrib(int metric) {
+__host__ __device__ constexpr int metric_contrib(int metric) {
   switch (metric) {
     case SD_M_KL: return C_KL;
     case SD_M_MANHATTAN: return C_ABS;
@@ -133,7 +143,7 @@ __device__ __forceinline__ T contrib(T a, T b, T p) {
   }
 }
 
-__host__ __device__ inline bool is_namm(int metric) {
+__host__ __device__ constexpr bool is_namm(int metric) {
   return metric >= SD_M_CANBERRA && metric <= SD_M_MINKOWSKI;
 }
 
