@@ -189,7 +189,9 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
           const int l = q + 32 * u + lane;
           const bool ok = l < nt;
           const int64_t j = j0 + l;
-          const T d = fused_value<T, M>(a, v[u], cv[u], ra0, ra1, rb0[u], rb1[u], flags);
+          uint32_t f = 0;
+          const T d = fused_value<T, M>(a, v[u], cv[u], ra0, ra1, rb0[u], rb1[u], f);
+          if (ok) flags |= f;  // lanes past the tile end evaluate a dummy cell
           if constexpr (KPL > 0) {
             top.offer(ok, d, j, a.topk);
           } else {
