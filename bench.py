@@ -208,7 +208,8 @@ def run_ours(args):
     dq = sd.to_device(queries, tdt, dev)
     ix = _lib.device_index(di)
     m, n = queries.n_rows, index.n_rows
-    out = torch.empty((m, n), dtype=tdt, device=dev)
+    ldo = (n + 3) // 4 * 4   # 16-byte aligned rows: the epilogue stores 4 cells per lane
+    out = torch.empty((m, ldo), dtype=tdt, device=dev)
     flags = _lib.new_flags(dev)
     stream = torch.cuda.current_stream(dev)
     sh = ctypes.c_void_p(stream.cuda_stream)
@@ -219,7 +220,7 @@ def run_ours(args):
         md = _lib.metric_struct(metric)
         ca, cb = _lib.csr_struct(dq), _lib.csr_struct(di)
         _lib.check(lib.sd_pairwise(ctypes.byref(ca), ctypes.byref(cb), ix.handle, _lib.dtype_code(tdt),
-                                   ctypes.byref(md), ctypes.byref(strat), out.data_ptr(), n, flags.data_ptr(),
+                                   ctypes.byref(md), ctypes.byref(strat), out.data_ptr(), ldo, flags.data_ptr(),
                                    ctypes.byref(rep), phases, sh), "sd_pairwise")
 
     def barrier():
@@ -327,7 +328,7 @@ def run_ours(args):
         rate, q, cores, dt, ref = cpu_reference_rate(index, queries, args.metric, sample=args.ref_queries,
                                                      budget_s=args.ref_budget)
         step(args.metric)
-        got = out[:q].double().cpu().numpy()
+        got = out[:q, :n].double().cpu().numpy()
         err = float(np.max(np.abs(got - ref) / (1e-5 + np.abs(ref)))) if ref.size else 0.0
         cpu = {"value": rate, "unit": "distances/s", "cores": cores, "kind": "port",
                "sample": f"{q} queries x {n} index rows ({dt:.1f}s, oracle numpy port, fp64)",

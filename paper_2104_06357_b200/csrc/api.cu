@@ -118,10 +118,10 @@ static int engine_pairwise(const sd_csr* a, const sd_csr* b, int dtype, const sd
   if (metric_two_pass(md->metric)) {
     SD_TRY(engine_pass(a, b, dtype, sr, md->p, 2, strat, out, ldo, report ? &r2 : nullptr, st));
   } else if (md->metric == SD_M_KL && a->n_rows > 0 && b->n_rows > 0) {
-    const int64_t n = b->n_rows;
-    SD_TRY(miss.alloc((dtype == SD_F64 ? 8 : 4) * size_t(a->n_rows) * size_t(n), st));
-    SD_TRY(fill(miss.ptr, a->n_rows, n, n, dtype, 0.0, st));
-    SD_TRY(engine_pass(a, b, dtype, SD_SR_MISS_COUNT, 0.0, 2, strat, miss.ptr, n, report ? &r2 : nullptr, st));
+    // miss counts share the output's leading dimension (expand reads both with ldo)
+    SD_TRY(miss.alloc((dtype == SD_F64 ? 8 : 4) * size_t(a->n_rows) * size_t(ldo), st));
+    SD_TRY(fill(miss.ptr, a->n_rows, b->n_rows, ldo, dtype, 0.0, st));
+    SD_TRY(engine_pass(a, b, dtype, SD_SR_MISS_COUNT, 0.0, 2, strat, miss.ptr, ldo, report ? &r2 : nullptr, st));
   }
   tm.end(PH_PASS2);
   if (report) {
@@ -130,7 +130,6 @@ static int engine_pairwise(const sd_csr* a, const sd_csr* b, int dtype, const sd
     report->chunks_executed = r1.chunks_executed + r2.chunks_executed;
   }
   if (md->metric == SD_M_KL && miss.ptr == nullptr) return SD_OK;
-  if (ldo != b->n_rows && miss.ptr) { set_error("kl engine path needs ldo == n"); return SD_E_INVALID; }
   tm.begin(PH_EXPANSION);
   SD_TRY(expand(out, a->n_rows, b->n_rows, ldo, dtype, md, a->n_cols, sa, sb, miss.ptr, flags, st));
   tm.end(PH_EXPANSION);

@@ -32,8 +32,7 @@ struct sd_index {
   int64_t n_tiles = 0;
   int dtype = 0;
   uint32_t* colptr = nullptr;  // [n_tiles * n_cols + 1]
-  uint16_t* post_j = nullptr;  // [nnz] row id within tile
-  void* post_v = nullptr;      // [nnz] value
+  void* post = nullptr;        // [nnz] Posting<T> (row id within tile, value)
   int64_t bytes = 0;
 };
 
@@ -55,7 +54,7 @@ template <typename T>
 __global__ void index_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                      const T* __restrict__ val, int64_t n_rows, int tile, int64_t n_cols,
                                      const uint32_t* __restrict__ colptr, uint32_t* cursor,
-                                     uint16_t* __restrict__ pj, T* __restrict__ pv) {
+                                     Posting<T>* __restrict__ post) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = warp; r < n_rows; r += nw) {
@@ -64,8 +63,11 @@ __global__ void index_scatter_kernel(const int64_t* __restrict__ ptr, const int3
     for (int64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
       const int64_t key = base + idx[e];
       const uint32_t pos = colptr[key] + atomicAdd(&cursor[key], 1u);
-      pj[pos] = uint16_t(r - t * tile);
-      pv[pos] = val[e];
+      Posting<T> q;
+      q.j = uint32_t(r - t * tile);
+      q.v = val[e];
+      if constexpr (sizeof(T) == 8) q.pad = 0;
+      post[pos] = q;
     }
   }
 }
@@ -81,13 +83,13 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
   ix->n_rows = b->n_rows; ix->n_cols = b->n_cols; ix->nnz = b->nnz;
   ix->tile = tile; ix->n_tiles = n_tiles; ix->dtype = dtype;
   auto fail = [&](int code) { sd_index_free(ix); return code; };
+  const size_t ps = dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>);
   if (cudaMalloc(&ix->colptr, sizeof(uint32_t) * (n_keys + 1)) != cudaSuccess ||
-      cudaMalloc(&ix->post_j, sizeof(uint16_t) * std::max<int64_t>(1, b->nnz)) != cudaSuccess ||
-      cudaMalloc(&ix->post_v, es * std::max<int64_t>(1, b->nnz)) != cudaSuccess) {
+      cudaMalloc(&ix->post, ps * std::max<int64_t>(1, b->nnz)) != cudaSuccess) {
     set_error("cudaMalloc failed for the inverted index");
     return fail(SD_E_CUDA);
   }
-  ix->bytes = int64_t(sizeof(uint32_t) * (n_keys + 1) + (2 + es) * b->nnz);
+  ix->bytes = int64_t(sizeof(uint32_t) * (n_keys + 1) + ps * b->nnz);
   Scratch counts;
   if (counts.alloc(sizeof(uint32_t) * (n_keys + 1), st) != SD_OK) return fail(SD_E_CUDA);
   if (cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (n_keys + 1), st) != cudaSuccess) return fail(SD_E_CUDA);
@@ -109,7 +111,7 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
     int rc = SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
       index_scatter_kernel<T><<<blocks, 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
                                                       b->n_rows, tile, b->n_cols, ix->colptr,
-                                                      counts.as<uint32_t>(), ix->post_j, static_cast<T*>(ix->post_v));
+                                                      counts.as<uint32_t>(), static_cast<Posting<T>*>(ix->post));
       SD_LAUNCH_CHECK();
       return SD_OK;
     });
@@ -236,7 +238,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     IsectArgs<T> args;
     args.a_ptr = a->indptr; args.a_idx = a->indices; args.a_val = static_cast<const T*>(a->values);
     args.m = m;
-    args.colptr = ix->colptr; args.pj = ix->post_j; args.pv = static_cast<const T*>(ix->post_v);
+    args.colptr = ix->colptr; args.post = static_cast<const Posting<T>*>(ix->post);
     args.tile = ix->tile; args.n_tiles = ix->n_tiles; args.n = ix->n_rows; args.n_cols = ix->n_cols;
     args.sa0 = static_cast<const T*>(sa.s[0]); args.sa1 = static_cast<const T*>(sa.s[1]);
     args.sb0 = static_cast<const T*>(sb.s[0]); args.sb1 = static_cast<const T*>(sb.s[1]);
@@ -259,8 +261,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
 int sd_index_free(sd_index* ix) {
   if (!ix) return SD_OK;
   if (ix->colptr) cudaFree(ix->colptr);
-  if (ix->post_j) cudaFree(ix->post_j);
-  if (ix->post_v) cudaFree(ix->post_v);
+  if (ix->post) cudaFree(ix->post);
   delete ix;
   return SD_OK;
 }

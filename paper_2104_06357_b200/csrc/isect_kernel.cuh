@@ -1,7 +1,6 @@
-// isect_kernel.cuh — the fused intersection kernel (see isect.cu for the
-// design).  Templated on <value type, metric, top-k slots per lane>; the
-// instantiations live in isect_f32.cu / isect_f64.cu so they compile in
-// parallel.
+// isect_kernel.cuh — the fused intersection kernel (design: isect.cu header).
+// Templated on <value type, metric, top-k slots per lane>; instantiations live
+// in isect_f32.cu / isect_f64.cu so they compile in parallel.
 #pragma once
 #include "common.cuh"
 #include "metric.cuh"
@@ -10,7 +9,11 @@
 
 namespace sd {
 
-// ---------------------------------------------------------------- kernel
+// One posting of the inverted index: row id within the tile + value, packed
+// so that a lane fetches it with a single 8-byte (fp32) / 16-byte (fp64) load.
+template <typename T> struct Posting;
+template <> struct __align__(8) Posting<float> { uint32_t j; float v; };
+template <> struct __align__(16) Posting<double> { uint32_t j; uint32_t pad; double v; };
 
 template <typename T>
 struct IsectArgs {
@@ -18,9 +21,8 @@ struct IsectArgs {
   const int32_t* a_idx;
   const T* a_val;
   int64_t m;
-  const uint32_t* colptr;
-  const uint16_t* pj;
-  const T* pv;
+  const uint32_t* colptr;   // [n_tiles * n_cols + 1]
+  const Posting<T>* post;
   int tile;
   int64_t n_tiles, n, n_cols;
   const T* sa0; const T* sa1; const T* sb0; const T* sb1;
@@ -42,6 +44,38 @@ struct IsectArgs {
 
 // columns whose first 32 postings are loaded before any is applied
 template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
+
+// 4 consecutive values through 16-byte shared/global accesses
+template <typename T> struct V4;
+template <> struct V4<float> {
+  __device__ __forceinline__ static void load(const float* p, float* v) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+  __device__ __forceinline__ static void store(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct V4<double> {
+  __device__ __forceinline__ static void load(const double* p, double* v) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    const double2 b = reinterpret_cast<const double2*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  __device__ __forceinline__ static void store(double* p, const double* v) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+  }
+};
+
+// Metrics whose value for a cell without any intersecting column is a
+// per-query constant once the query row is non-empty (the common case on
+// sparse data): the epilogue then skips the division entirely.
+template <int M>
+__host__ __device__ constexpr bool sparse_result() {
+  return M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_JACCARD || M == SD_M_DOT ||
+         M == SD_M_RUSSELRAO || M == SD_M_HELLINGER;
+}
 
 template <typename T, int M>
 __device__ __forceinline__ T fused_value(const IsectArgs<T>& a, T acc, T cnt, T ra0, T ra1, T rb0, T rb1,
@@ -79,6 +113,7 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
   T* cnt = acc + TJ;
   const T p = a.p;
   const int64_t total_items = a.item_off[a.m];
+  const bool vec_out = KPL == 0 && (a.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
   uint32_t flags = 0;
 
   for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
@@ -100,6 +135,14 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
     const T ra0 = a.sa0 ? a.sa0[i] : T(0);
     const T ra1 = a.sa1 ? a.sa1[i] : T(0);
+    // value of a cell without intersections when the query row is non-empty
+    bool fast_zero = false;
+    T zero_val = T(0);
+    if constexpr (sparse_result<M>()) {
+      fast_zero = (M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_JACCARD) ? ra0 > T(0) : true;
+      uint32_t f = 0;
+      zero_val = expand_cell_t<M, T>(T(0), ra0, ra1, T(1), T(1), a.k, a.p, f);
+    }
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
     if constexpr (KPL > 0) top.init();
 
@@ -116,27 +159,24 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
       uint32_t pe = valid ? cp[c + 1] : 0u;
       for (int64_t base = abeg; base < aend; base += 32) {
         const int ncol = int(tmin<int64_t>(32, aend - base));
-        const uint32_t cur_pb = pb, cur_pe = pe;
+        const uint32_t cur_pb = pb;
         const T cur_av = av;
+        const unsigned long_mask = __ballot_sync(FULL, pe - pb > 32u);
+        const uint32_t cur_pe = pe;
         // next batch's columns (independent of this batch's postings)
         e = base + 32 + lane;
         valid = e < aend;
         c = valid ? a.a_idx[e] : 0;
         av = valid ? a.a_val[e] : T(0);
         for (int q0 = 0; q0 < ncol; q0 += U) {
-          int jl[U];
-          T y[U];
+          Posting<T> ps[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
             const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
             const uint32_t pp = b0 + lane;
-            jl[u] = -1;
-            y[u] = T(0);
-            if (q0 + u < ncol && pp < b1) {
-              jl[u] = a.pj[pp];
-              y[u] = a.pv[pp];
-            }
+            ps[u].j = 0xffffffffu;
+            if (q0 + u < ncol && pp < b1) ps[u] = a.post[pp];
           }
           if (q0 + U >= ncol) {  // last group of this batch: start the next batch's colptr loads
             pb = valid ? cp[c] : 0u;
@@ -146,56 +186,72 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
           for (int u = 0; u < U; ++u) {
             if (q0 + u < ncol) {
               const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
-              if (jl[u] >= 0) {
-                acc[jl[u]] = add_rn(acc[jl[u]], contrib<CK, T>(x, y[u], p));
-                if constexpr (KL) cnt[jl[u]] = add_rn(cnt[jl[u]], T(1));
+              if (ps[u].j != 0xffffffffu) {
+                acc[ps[u].j] = add_rn(acc[ps[u].j], contrib<CK, T>(x, ps[u].v, p));
+                if constexpr (KL) cnt[ps[u].j] = add_rn(cnt[ps[u].j], T(1));
               }
-              const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
-              const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
-              for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {  // columns with > 32 postings in this tile
-                const int j2 = a.pj[p2];
-                acc[j2] = add_rn(acc[j2], contrib<CK, T>(x, a.pv[p2], p));
-                if constexpr (KL) cnt[j2] = add_rn(cnt[j2], T(1));
+              if (long_mask & (1u << ((q0 + u) & 31))) {  // > 32 postings of this column in this tile
+                const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
+                const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
+                for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
+                  const Posting<T> q2 = a.post[p2];
+                  acc[q2.j] = add_rn(acc[q2.j], contrib<CK, T>(x, q2.v, p));
+                  if constexpr (KL) cnt[q2.j] = add_rn(cnt[q2.j], T(1));
+                }
               }
               __syncwarp();
             }
           }
         }
       }
-      // epilogue over the tile's cells, 4 cells per lane in flight; the
-      // accumulator is re-zeroed as it is read
-      for (int q = 0; q < nt; q += 128) {
-        T v[4], cv[4], rb0[4], rb1[4];
+      // epilogue: each lane finishes 4 consecutive cells per step (16-byte
+      // shared/global accesses); the accumulator is re-zeroed as it is read
+      T* orow = KPL == 0 ? a.out + i * a.ldo + j0 : nullptr;
+      const T zero4[4] = {T(0), T(0), T(0), T(0)};
+      for (int qb = 0; qb < nt; qb += 128) {  // warp-uniform trip count (top-k offers are collective)
+        const int q = qb + 4 * lane;
+        const bool full = q + 3 < nt;
+        T v[4] = {T(0), T(0), T(0), T(0)}, cv[4] = {T(0), T(0), T(0), T(0)};
+        T b0[4] = {T(0), T(0), T(0), T(0)}, b1[4] = {T(0), T(0), T(0), T(0)};
+        if (full) {
+          V4<T>::load(acc + q, v);
+          V4<T>::store(acc + q, zero4);
+          if constexpr (KL) { V4<T>::load(cnt + q, cv); V4<T>::store(cnt + q, zero4); }
+          if constexpr (SB0) V4<T>::load(a.sb0 + j0 + q, b0);
+          if constexpr (SB1) V4<T>::load(a.sb1 + j0 + q, b1);
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int l = q + 32 * u + lane;
-          const bool ok = l < nt;
-          v[u] = ok ? acc[l] : T(0);
-          cv[u] = T(0);
-          if constexpr (KL) cv[u] = ok ? cnt[l] : T(0);
-          rb0[u] = (SB0 && ok) ? a.sb0[j0 + l] : T(0);
-          rb1[u] = (SB1 && ok) ? a.sb1[j0 + l] : T(0);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int l = q + 32 * u + lane;
-          if (l < nt) {
-            acc[l] = T(0);
-            if constexpr (KL) cnt[l] = T(0);
+          for (int u = 0; u < 4; ++u) {
+            if (q + u < nt) {
+              v[u] = acc[q + u];
+              acc[q + u] = T(0);
+              if constexpr (KL) { cv[u] = cnt[q + u]; cnt[q + u] = T(0); }
+              if constexpr (SB0) b0[u] = a.sb0[j0 + q + u];
+              if constexpr (SB1) b1[u] = a.sb1[j0 + q + u];
+            }
           }
         }
+        T r[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int l = q + 32 * u + lane;
-          const bool ok = l < nt;
-          const int64_t j = j0 + l;
-          uint32_t f = 0;
-          const T d = fused_value<T, M>(a, v[u], cv[u], ra0, ra1, rb0[u], rb1[u], f);
-          if (ok) flags |= f;  // lanes past the tile end evaluate a dummy cell
-          if constexpr (KPL > 0) {
-            top.offer(ok, d, j, a.topk);
+          if (fast_zero && v[u] == T(0)) {
+            r[u] = zero_val;
           } else {
-            if (ok) a.out[i * a.ldo + j] = d;
+            uint32_t f = 0;
+            r[u] = fused_value<T, M>(a, v[u], cv[u], ra0, ra1, b0[u], b1[u], f);
+            if (q + u < nt) flags |= f;  // lanes past the tile end evaluate a dummy cell
+          }
+        }
+        if constexpr (KPL > 0) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) top.offer(q + u < nt, r[u], j0 + q + u, a.topk);
+        } else {
+          if (full && vec_out) {
+            V4<T>::store(orow + q, r);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (q + u < nt) orow[q + u] = r[u];
           }
         }
       }
@@ -228,7 +284,6 @@ __global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __re
     top.store(k, od + i * k, oi + i * k, base);
   }
 }
-
 
 template <typename T, int M, int KPL>
 int launch_isect_kernel(IsectArgs<T>& args, int W, cudaStream_t st) {

@@ -224,7 +224,9 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
     fused = strategy is None or (isinstance(strategy, str) and strategy == "auto")
     report = _engine_report(da, db, passes, name, strategy, a, b)
     host_out = out
-    out = torch.empty((a.n_rows, b.n_rows), dtype=tdt, device=da.device)
+    ldo = (b.n_rows + 3) // 4 * 4   # 16-byte aligned rows let the kernel store 4 cells per lane
+    out_buf = torch.empty((a.n_rows, ldo), dtype=tdt, device=da.device)
+    out = out_buf[:, :b.n_rows]
     flags = _lib.new_flags(da.device)
     md = _lib.metric_struct(name, p, strict, pre_transformed=transform is not None)
     phases = (ctypes.c_float * 4)()
@@ -238,7 +240,7 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
         index = None
     rep = _lib.SdReport()
     _lib.check(lib.sd_pairwise(ctypes.byref(ca), ctypes.byref(cb), index, _lib.dtype_code(tdt), ctypes.byref(md),
-                               ctypes.byref(strat), out.data_ptr() if out.numel() else None, b.n_rows,
+                               ctypes.byref(strat), out_buf.data_ptr() if out.numel() else None, ldo,
                                flags.data_ptr(), ctypes.byref(rep), phases, _lib.stream_handle(da.device)),
                "sd_pairwise")
     if check_flags:
