@@ -104,8 +104,8 @@ static int engine_pairwise(const sd_csr* a, const sd_csr* b, int dtype, const sd
   const size_t es = dtype == SD_F64 ? 8 : 4;
   tm.begin(PH_NORMS);
   if (ns > 0 && !is_namm(md->metric) && md->metric != SD_M_KL) {
-    SD_TRY(sabuf.alloc(es * ns * std::max<int64_t>(1, a->n_rows), st));
-    SD_TRY(sbbuf.alloc(es * ns * std::max<int64_t>(1, b->n_rows), st));
+    SD_TRY(sabuf.alloc(es * ns * stats_stride(std::max<int64_t>(1, a->n_rows)), st));
+    SD_TRY(sbbuf.alloc(es * ns * stats_stride(std::max<int64_t>(1, b->n_rows)), st));
     SD_TRY(metric_stats(a, dtype, md, true, sabuf.ptr, &sa, st));
     SD_TRY(metric_stats(b, dtype, md, false, sbbuf.ptr, &sb, st));
   }

@@ -40,7 +40,8 @@ int metric_stats(const sd_csr* m, int dtype, const sd_metric_desc* md, bool a_si
   const size_t es = dtype == SD_F64 ? 8 : 4;
   char* b = static_cast<char*>(buf);
   const int64_t n = m->n_rows;
-  auto slot = [&](int q) { return static_cast<void*>(b + size_t(q) * size_t(n) * es); };
+  // slots start on 32-byte boundaries: the fused epilogue reads them 4 values at a time
+  auto slot = [&](int q) { return static_cast<void*>(b + size_t(q) * size_t(stats_stride(n)) * es); };
   switch (md->metric) {
     case SD_M_CORRELATION:
       SD_TRY(row_stat(m, dtype, SD_STAT_SUM, 0, 0.0, slot(0), st));

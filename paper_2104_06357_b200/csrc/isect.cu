@@ -19,6 +19,7 @@
 //
 // HBM traffic is the output write plus posting reads, which stay L2-resident
 // per tile (DESIGN.md §7 byte model).
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include "common.cuh"
 #include "metric.cuh"
@@ -38,7 +39,13 @@ struct sd_index {
 
 namespace sd {
 
-int default_tile(int dtype) { return dtype == SD_F64 ? 2048 : 4096; }
+int default_tile(int dtype) {
+  if (const char* e = getenv("SD_TILE")) {  // experiment override
+    const int t = atoi(e);
+    if (t >= 128 && t <= 65536 && t % 128 == 0) return dtype == SD_F64 ? t / 2 : t;
+  }
+  return dtype == SD_F64 ? 2048 : 4096;
+}
 
 __global__ void index_count_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                    int64_t n_rows, int tile, int64_t n_cols, uint32_t* counts) {
@@ -126,9 +133,9 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
 // so that every item costs about total/(8·warps) — a power-law query of
 // degree 25k is spread over up to n_tiles warps instead of serialising on one.
 __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ ptr, int64_t m, int64_t n_tiles,
-                                                    int64_t warps, int64_t epi_cost, int32_t* __restrict__ order,
-                                                    int32_t* __restrict__ tpi, int64_t* __restrict__ item_off,
-                                                    int32_t* __restrict__ item_pos) {
+                                                    int64_t warps, int64_t epi_cost, int tile_major,
+                                                    int32_t* __restrict__ order, int32_t* __restrict__ tpi,
+                                                    int64_t* __restrict__ item_off, int32_t* __restrict__ item_pos) {
   __shared__ unsigned int hist[64];
   __shared__ unsigned int base[64];
   __shared__ unsigned long long total;
@@ -156,6 +163,11 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     order[atomicAdd(&base[63 - b], 1u)] = int32_t(r);
   }
   __syncthreads();
+  if (tile_major) {  // items (tile t, position p) ordered tile-major: item = t * m + p
+    for (int64_t q = threadIdx.x; q < m; q += blockDim.x) { tpi[q] = 1; item_off[q] = q * n_tiles; }
+    if (threadIdx.x == 0) item_off[m] = m * n_tiles;
+    return;
+  }
   const int64_t target = tmax<int64_t>(1, int64_t(total) * n_tiles / tmax<int64_t>(1, warps * 8));
   // contiguous chunk per thread: items per position, then a block scan
   const int64_t chunk = (m + blockDim.x - 1) / blockDim.x;
@@ -192,10 +204,10 @@ int isect_stats(const sd_csr* a, const sd_csr* b, int dtype, const sd_metric_des
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t ns = metric_stats_count(md->metric);
   if (ns == 0) return SD_OK;
-  SD_TRY(sa_buf.alloc(es * ns * std::max<int64_t>(1, a->n_rows), st));
+  SD_TRY(sa_buf.alloc(es * ns * stats_stride(std::max<int64_t>(1, a->n_rows)), st));
   SD_TRY(metric_stats(a, dtype, md, true, sa_buf.ptr, sa, st));
   if (md->metric != SD_M_KL) {
-    SD_TRY(sb_buf.alloc(es * ns * std::max<int64_t>(1, b->n_rows), st));
+    SD_TRY(sb_buf.alloc(es * ns * stats_stride(std::max<int64_t>(1, b->n_rows)), st));
     SD_TRY(metric_stats(b, dtype, md, false, sb_buf.ptr, sb, st));
   }
   return SD_OK;
@@ -227,8 +239,11 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   SD_TRY(item_pos.alloc(sizeof(int32_t) * max_items, st));
   SD_TRY(counter.alloc(sizeof(unsigned int), st));
   SD_CUDA_TRY(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int), st));
-  plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, warps, ix->tile / 16, order.as<int32_t>(),
-                                  tpi.as<int32_t>(), item_off.as<int64_t>(), item_pos.as<int32_t>());
+  const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
+  const int tile_major = pe ? atoi(pe) : 0;
+  plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, warps, ix->tile / 16, tile_major,
+                                  order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
+                                  item_pos.as<int32_t>());
   SD_LAUNCH_CHECK();
   if (topk > 0) {
     SD_TRY(cand_d.alloc(es * size_t(max_items) * topk, st));
@@ -245,6 +260,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.order = order.as<int32_t>(); args.tpi = tpi.as<int32_t>();
     args.item_off = item_off.as<int64_t>(); args.item_pos = item_pos.as<int32_t>();
     args.counter = counter.as<unsigned int>();
+    args.tile_major = tile_major;
     args.strict = md->strict;
     args.k = T(a->n_cols); args.p = T(md->p);
     args.out = static_cast<T*>(out); args.ldo = ldo; args.flags = flags;

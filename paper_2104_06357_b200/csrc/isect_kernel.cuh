@@ -32,6 +32,7 @@ struct IsectArgs {
   const int64_t* item_off;  // items of position p: [item_off[p], item_off[p+1])
   const int32_t* item_pos;  // item -> plan position
   unsigned int* counter;
+  int tile_major;           // items are (tile, position) pairs in tile-major order
   int strict;
   T k, p;
   T* out;
@@ -127,11 +128,19 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
     if (lane == 0) item = atomicAdd(a.counter, 1u);
     item = __shfl_sync(FULL, item, 0);
     if (int64_t(item) >= total_items) break;
-    const int pos = a.item_pos[item];
+    int pos;
+    int64_t t0, t1;
+    if (a.tile_major) {
+      t0 = int64_t(item) / a.m;
+      pos = int(int64_t(item) - t0 * a.m);
+      t1 = t0 + 1;
+    } else {
+      pos = a.item_pos[item];
+      const int64_t tpi = a.tpi[pos];
+      t0 = (int64_t(item) - a.item_off[pos]) * tpi;
+      t1 = tmin<int64_t>(a.n_tiles, t0 + tpi);
+    }
     const int64_t i = a.order[pos];
-    const int64_t tpi = a.tpi[pos];
-    const int64_t t0 = (int64_t(item) - a.item_off[pos]) * tpi;
-    const int64_t t1 = tmin<int64_t>(a.n_tiles, t0 + tpi);
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
     const T ra0 = a.sa0 ? a.sa0[i] : T(0);
     const T ra1 = a.sa1 ? a.sa1[i] : T(0);
@@ -268,18 +277,22 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
 template <typename T, int KPL>
 __global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __restrict__ ci,
                                    const int32_t* __restrict__ order, const int64_t* __restrict__ item_off,
-                                   int64_t m, int k, int64_t base, T* __restrict__ od, int64_t* __restrict__ oi) {
+                                   int64_t m, int k, int tile_major, int64_t n_tiles, int64_t base,
+                                   T* __restrict__ od, int64_t* __restrict__ oi) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t p = warp; p < m; p += nw) {
     WarpTopK<T, KPL> top;
     top.init();
-    for (int64_t it = item_off[p]; it < item_off[p + 1]; ++it)
+    const int64_t n_lists = tile_major ? n_tiles : item_off[p + 1] - item_off[p];
+    for (int64_t l = 0; l < n_lists; ++l) {
+      const int64_t it = tile_major ? l * m + p : item_off[p] + l;
       for (int q = 0; q < k; q += 32) {
         const int j = q + int(lane_id());
         const bool ok = j < k;
         top.offer(ok, ok ? cd[it * k + j] : T(0), ok ? ci[it * k + j] : 0, k);
       }
+    }
     const int64_t i = order[p];
     top.store(k, od + i * k, oi + i * k, base);
   }
@@ -330,10 +343,10 @@ int launch_isect_metric(IsectArgs<T>& args, int W, cudaStream_t st) {
     const int blocks = int(std::min<int64_t>((a.m * 32 + 255) / 256, int64_t(num_sms()) * 16));    \
     if (a.topk <= 32)                                                                               \
       merge_items_kernel<T, 1><<<blocks, 256, 0, st>>>(a.cand_d, a.cand_i, a.order, a.item_off,    \
-                                                        a.m, a.topk, base, od, oi);                 \
+                                                        a.m, a.topk, a.tile_major, a.n_tiles, base, od, oi); \
     else                                                                                            \
       merge_items_kernel<T, 4><<<blocks, 256, 0, st>>>(a.cand_d, a.cand_i, a.order, a.item_off,    \
-                                                        a.m, a.topk, base, od, oi);                 \
+                                                        a.m, a.topk, a.tile_major, a.n_tiles, base, od, oi); \
     SD_LAUNCH_CHECK();                                                                              \
     return SD_OK;                                                                                   \
   }

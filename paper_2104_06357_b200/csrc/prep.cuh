@@ -4,6 +4,9 @@
 
 namespace sd {
 
+// rows per statistic slot, rounded so every slot is 32-byte aligned
+inline int64_t stats_stride(int64_t n) { return (n + 3) & ~int64_t(3); }
+
 struct Stats {  // per-row statistics the metric epilogue reads (metric.cuh layout)
   const void* s[3] = {nullptr, nullptr, nullptr};
 };
