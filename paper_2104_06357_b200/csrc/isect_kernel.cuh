@@ -69,6 +69,41 @@ template <> struct V4<double> {
   }
 };
 
+// Explicit shared-window accesses (32-bit addresses): generic pointers into the
+// dynamic shared buffer made the compiler rebuild the cluster window address
+// for every access.
+__device__ __forceinline__ float lds(uint32_t a, float) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds(uint32_t a, double) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void lds4(uint32_t a, float* v) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void lds4(uint32_t a, double* v) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a) : "memory");
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16) : "memory");
+}
+__device__ __forceinline__ void sts4_zero(uint32_t a, float) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" :: "r"(a), "f"(0.f) : "memory");
+}
+__device__ __forceinline__ void sts4_zero(uint32_t a, double) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a), "d"(0.0) : "memory");
+  asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a + 16), "d"(0.0) : "memory");
+}
+
 // Metrics whose value for a cell without any intersecting column is a
 // per-query constant once the query row is non-empty (the common case on
 // sparse data): the epilogue then skips the division entirely.
@@ -110,16 +145,17 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int TJ = a.tile;
-  T* acc = reinterpret_cast<T*>(smem) + size_t(warp) * TJ * (KL ? 2 : 1);
-  T* cnt = acc + TJ;
+  constexpr uint32_t ES = sizeof(T);
+  const uint32_t acc_s = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(warp) * TJ * ES * (KL ? 2u : 1u);
+  const uint32_t cnt_s = acc_s + uint32_t(TJ) * ES;
   const T p = a.p;
   const int64_t total_items = a.item_off[a.m];
   const bool vec_out = KPL == 0 && (a.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
   uint32_t flags = 0;
 
   for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
-    acc[q] = T(0);
-    if constexpr (KL) cnt[q] = T(0);
+    sts(acc_s + q * ES, T(0));
+    if constexpr (KL) sts(cnt_s + q * ES, T(0));
   }
   __syncwarp();
 
@@ -196,16 +232,19 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
             if (q0 + u < ncol) {
               const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
               if (ps[u].j != 0xffffffffu) {
-                acc[ps[u].j] = add_rn(acc[ps[u].j], contrib<CK, T>(x, ps[u].v, p));
-                if constexpr (KL) cnt[ps[u].j] = add_rn(cnt[ps[u].j], T(1));
+                const T cval = contrib<CK, T>(x, ps[u].v, p);
+                const uint32_t ad = acc_s + ps[u].j * ES;
+                sts(ad, add_rn(lds(ad, T(0)), cval));
+                if constexpr (KL) sts(cnt_s + ps[u].j * ES, add_rn(lds(cnt_s + ps[u].j * ES, T(0)), T(1)));
               }
               if (long_mask & (1u << ((q0 + u) & 31))) {  // > 32 postings of this column in this tile
                 const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
                 const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
                 for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
                   const Posting<T> q2 = a.post[p2];
-                  acc[q2.j] = add_rn(acc[q2.j], contrib<CK, T>(x, q2.v, p));
-                  if constexpr (KL) cnt[q2.j] = add_rn(cnt[q2.j], T(1));
+                  const uint32_t ad = acc_s + q2.j * ES;
+                  sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, q2.v, p)));
+                  if constexpr (KL) sts(cnt_s + q2.j * ES, add_rn(lds(cnt_s + q2.j * ES, T(0)), T(1)));
                 }
               }
               __syncwarp();
@@ -216,25 +255,24 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
       // epilogue: each lane finishes 4 consecutive cells per step (16-byte
       // shared/global accesses); the accumulator is re-zeroed as it is read
       T* orow = KPL == 0 ? a.out + i * a.ldo + j0 : nullptr;
-      const T zero4[4] = {T(0), T(0), T(0), T(0)};
       for (int qb = 0; qb < nt; qb += 128) {  // warp-uniform trip count (top-k offers are collective)
         const int q = qb + 4 * lane;
         const bool full = q + 3 < nt;
         T v[4] = {T(0), T(0), T(0), T(0)}, cv[4] = {T(0), T(0), T(0), T(0)};
         T b0[4] = {T(0), T(0), T(0), T(0)}, b1[4] = {T(0), T(0), T(0), T(0)};
         if (full) {
-          V4<T>::load(acc + q, v);
-          V4<T>::store(acc + q, zero4);
-          if constexpr (KL) { V4<T>::load(cnt + q, cv); V4<T>::store(cnt + q, zero4); }
+          lds4(acc_s + q * ES, v);
+          sts4_zero(acc_s + q * ES, T(0));
+          if constexpr (KL) { lds4(cnt_s + q * ES, cv); sts4_zero(cnt_s + q * ES, T(0)); }
           if constexpr (SB0) V4<T>::load(a.sb0 + j0 + q, b0);
           if constexpr (SB1) V4<T>::load(a.sb1 + j0 + q, b1);
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (q + u < nt) {
-              v[u] = acc[q + u];
-              acc[q + u] = T(0);
-              if constexpr (KL) { cv[u] = cnt[q + u]; cnt[q + u] = T(0); }
+              v[u] = lds(acc_s + (q + u) * ES, T(0));
+              sts(acc_s + (q + u) * ES, T(0));
+              if constexpr (KL) { cv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
               if constexpr (SB0) b0[u] = a.sb0[j0 + q + u];
               if constexpr (SB1) b1[u] = a.sb1[j0 + q + u];
             }
