@@ -228,7 +228,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   if (m >= (int64_t(1) << 31)) { set_error("too many query rows"); return SD_E_INVALID; }
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t per_warp = int64_t(ix->tile) * int64_t(es) * (ck == C_KL ? 2 : 1);
-  const int W = int(std::min<int64_t>(16, (smem_optin_bytes() - 2048) / per_warp));
+  const int W = int(std::min<int64_t>(ISECT_MAX_WARPS, (smem_optin_bytes() - 2048) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const int64_t warps = int64_t(num_sms()) * W;
   const int64_t max_items = m * ix->n_tiles;

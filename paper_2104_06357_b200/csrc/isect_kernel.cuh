@@ -43,6 +43,10 @@ struct IsectArgs {
   int64_t* cand_i;
 };
 
+// warps per CTA (one CTA per SM: 14 x 16 KB accumulators = 224 KB); capping
+// the CTA at 448 threads gives each thread up to 144 registers
+constexpr int ISECT_MAX_WARPS = 14;
+
 // columns whose first 32 postings are loaded before any is applied
 template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
 
@@ -68,6 +72,25 @@ template <> struct V4<double> {
     reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
   }
 };
+
+// read-only 8/16-byte posting fetch (ld.global.nc)
+__device__ __forceinline__ Posting<float> load_posting(const Posting<float>* p) {
+  uint2 r;
+  asm("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  Posting<float> q;
+  q.j = r.x;
+  q.v = __uint_as_float(r.y);
+  return q;
+}
+__device__ __forceinline__ Posting<double> load_posting(const Posting<double>* p) {
+  unsigned long long a, b;
+  asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  Posting<double> q;
+  q.j = uint32_t(a);
+  q.pad = 0;
+  q.v = __longlong_as_double((long long)b);
+  return q;
+}
 
 // Explicit shared-window accesses (32-bit addresses): generic pointers into the
 // dynamic shared buffer made the compiler rebuild the cluster window address
@@ -133,7 +156,7 @@ __device__ __forceinline__ T fused_value(const IsectArgs<T>& a, T acc, T cnt, T 
 }
 
 template <typename T, int M, int KPL>
-__global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
+__global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const IsectArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CK = metric_contrib(M);
   constexpr bool KL = CK == C_KL;
@@ -146,8 +169,13 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
   const int lane = threadIdx.x & 31;
   const int TJ = a.tile;
   constexpr uint32_t ES = sizeof(T);
-  const uint32_t acc_s = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(warp) * TJ * ES * (KL ? 2u : 1u);
+  // opaque copies: keeps the accumulator base and the posting pointer in
+  // registers instead of letting the compiler rebuild them per access
+  uint32_t acc_s;
+  asm volatile("mov.b32 %0, %1;" : "=r"(acc_s)
+               : "r"(uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(warp) * TJ * ES * (KL ? 2u : 1u)));
   const uint32_t cnt_s = acc_s + uint32_t(TJ) * ES;
+  const Posting<T>* __restrict__ post = a.post;
   const T p = a.p;
   const int64_t total_items = a.item_off[a.m];
   const bool vec_out = KPL == 0 && (a.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
@@ -221,7 +249,7 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
             const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
             const uint32_t pp = b0 + lane;
             ps[u].j = 0xffffffffu;
-            if (q0 + u < ncol && pp < b1) ps[u] = a.post[pp];
+            if (q0 + u < ncol && pp < b1) ps[u] = load_posting(post + pp);
           }
           if (q0 + U >= ncol) {  // last group of this batch: start the next batch's colptr loads
             pb = valid ? cp[c] : 0u;
@@ -241,7 +269,7 @@ __global__ void __launch_bounds__(512) isect_kernel(const IsectArgs<T> a) {
                 const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
                 const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
                 for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
-                  const Posting<T> q2 = a.post[p2];
+                  const Posting<T> q2 = load_posting(post + p2);
                   const uint32_t ad = acc_s + q2.j * ES;
                   sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, q2.v, p)));
                   if constexpr (KL) sts(cnt_s + q2.j * ES, add_rn(lds(cnt_s + q2.j * ES, T(0)), T(1)));
