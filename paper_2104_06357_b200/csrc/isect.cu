@@ -133,7 +133,7 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
 // so that every item costs about total/(8·warps) — a power-law query of
 // degree 25k is spread over up to n_tiles warps instead of serialising on one.
 __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ ptr, int64_t m, int64_t n_tiles,
-                                                    int64_t warps, int64_t epi_cost, int tile_major,
+                                                    int64_t band, int64_t warps, int64_t epi_cost, int tile_major,
                                                     int32_t* __restrict__ order, int32_t* __restrict__ tpi,
                                                     int64_t* __restrict__ item_off, int32_t* __restrict__ item_pos) {
   __shared__ unsigned int hist[64];
@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     if (threadIdx.x == 0) item_off[m] = m * n_tiles;
     return;
   }
-  const int64_t target = tmax<int64_t>(1, int64_t(total) * n_tiles / tmax<int64_t>(1, warps * 8));
+  // items of one band (the list repeats for every band of `band` tiles)
+  const int64_t target = tmax<int64_t>(1, int64_t(total) * band / tmax<int64_t>(1, warps * 8));
   // contiguous chunk per thread: items per position, then a block scan
   const int64_t chunk = (m + blockDim.x - 1) / blockDim.x;
   const int64_t lo = tmin<int64_t>(m, int64_t(threadIdx.x) * chunk), hi = tmin<int64_t>(m, lo + chunk);
@@ -176,9 +177,9 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
   for (int64_t q = lo; q < hi; ++q) {
     const int64_t r = order[q];
     const int64_t cost = ptr[r + 1] - ptr[r] + epi_cost;
-    const int64_t t = tmin<int64_t>(n_tiles, tmax<int64_t>(1, target / cost));
+    const int64_t t = tmin<int64_t>(band, tmax<int64_t>(1, target / cost));
     tpi[q] = int32_t(t);
-    sum += (n_tiles + t - 1) / t;
+    sum += (band + t - 1) / t;
   }
   part[threadIdx.x] = sum;
   __syncthreads();
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
   int64_t off = part[threadIdx.x];
   for (int64_t q = lo; q < hi; ++q) {
     item_off[q] = off;
-    const int64_t cnt = (n_tiles + tpi[q] - 1) / tpi[q];
+    const int64_t cnt = (band + tpi[q] - 1) / tpi[q];
     for (int64_t it = 0; it < cnt; ++it) item_pos[off + it] = int32_t(q);
     off += cnt;
   }
@@ -231,7 +232,9 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   const int W = int(std::min<int64_t>(ISECT_MAX_WARPS, (smem_optin_bytes() - 2048) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const int64_t warps = int64_t(num_sms()) * W;
-  const int64_t max_items = m * ix->n_tiles;
+  const char* be0 = getenv("SD_ISECT_BAND");
+  const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : ix->n_tiles));
+  const int64_t max_items = m * band0 * ((ix->n_tiles + band0 - 1) / band0);
   Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
   SD_TRY(order.alloc(sizeof(int32_t) * m, st));
   SD_TRY(tpi.alloc(sizeof(int32_t) * m, st));
@@ -241,7 +244,9 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   SD_CUDA_TRY(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int), st));
   const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
   const int tile_major = pe ? atoi(pe) : 0;
-  plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, warps, ix->tile / 16, tile_major,
+  const char* be = getenv("SD_ISECT_BAND");  // tiles per band (L2-resident posting working set)
+  const int64_t band = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be ? atoll(be) : ix->n_tiles));
+  plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
                                   order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
                                   item_pos.as<int32_t>());
   SD_LAUNCH_CHECK();
@@ -261,6 +266,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.item_off = item_off.as<int64_t>(); args.item_pos = item_pos.as<int32_t>();
     args.counter = counter.as<unsigned int>();
     args.tile_major = tile_major;
+    args.band = band;
     args.strict = md->strict;
     args.k = T(a->n_cols); args.p = T(md->p);
     args.out = static_cast<T*>(out); args.ldo = ldo; args.flags = flags;

@@ -33,6 +33,7 @@ struct IsectArgs {
   const int32_t* item_pos;  // item -> plan position
   unsigned int* counter;
   int tile_major;           // items are (tile, position) pairs in tile-major order
+  int64_t band;             // tiles per band (band-major plan)
   int strict;
   T k, p;
   T* out;
@@ -177,7 +178,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
   const uint32_t cnt_s = acc_s + uint32_t(TJ) * ES;
   const Posting<T>* __restrict__ post = a.post;
   const T p = a.p;
-  const int64_t total_items = a.item_off[a.m];
+  const int64_t band_items = a.item_off[a.m];  // written by plan_kernel
+  const int64_t total_items = a.tile_major ? band_items : band_items * ((a.n_tiles + a.band - 1) / a.band);
   const bool vec_out = KPL == 0 && (a.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
   uint32_t flags = 0;
 
@@ -199,10 +201,13 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
       pos = int(int64_t(item) - t0 * a.m);
       t1 = t0 + 1;
     } else {
-      pos = a.item_pos[item];
+      // band-major items: every band of `band` tiles repeats the same item list
+      const int64_t band = int64_t(item) / band_items;
+      const int64_t r = int64_t(item) - band * band_items;
+      pos = a.item_pos[r];
       const int64_t tpi = a.tpi[pos];
-      t0 = (int64_t(item) - a.item_off[pos]) * tpi;
-      t1 = tmin<int64_t>(a.n_tiles, t0 + tpi);
+      t0 = band * a.band + (r - a.item_off[pos]) * tpi;
+      t1 = tmin<int64_t>(tmin<int64_t>(a.n_tiles, (band + 1) * a.band), t0 + tpi);
     }
     const int64_t i = a.order[pos];
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
@@ -255,9 +260,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
             pb = valid ? cp[c] : 0u;
             pe = valid ? cp[c + 1] : 0u;
           }
+          if (ncol == 32 && long_mask == 0u) {
+            // fast path: a full batch without long posting lists (warp-uniform)
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (q0 + u < ncol) {
+            for (int u = 0; u < U; ++u) {
               const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
               if (ps[u].j != 0xffffffffu) {
                 const T cval = contrib<CK, T>(x, ps[u].v, p);
@@ -265,17 +271,31 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
                 sts(ad, add_rn(lds(ad, T(0)), cval));
                 if constexpr (KL) sts(cnt_s + ps[u].j * ES, add_rn(lds(cnt_s + ps[u].j * ES, T(0)), T(1)));
               }
-              if (long_mask & (1u << ((q0 + u) & 31))) {  // > 32 postings of this column in this tile
-                const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
-                const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
-                for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
-                  const Posting<T> q2 = load_posting(post + p2);
-                  const uint32_t ad = acc_s + q2.j * ES;
-                  sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, q2.v, p)));
-                  if constexpr (KL) sts(cnt_s + q2.j * ES, add_rn(lds(cnt_s + q2.j * ES, T(0)), T(1)));
-                }
-              }
               __syncwarp();
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (q0 + u < ncol) {
+                const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
+                if (ps[u].j != 0xffffffffu) {
+                  const T cval = contrib<CK, T>(x, ps[u].v, p);
+                  const uint32_t ad = acc_s + ps[u].j * ES;
+                  sts(ad, add_rn(lds(ad, T(0)), cval));
+                  if constexpr (KL) sts(cnt_s + ps[u].j * ES, add_rn(lds(cnt_s + ps[u].j * ES, T(0)), T(1)));
+                }
+                if (long_mask & (1u << ((q0 + u) & 31))) {  // > 32 postings of this column in this tile
+                  const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
+                  const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
+                  for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
+                    const Posting<T> q2 = load_posting(post + p2);
+                    const uint32_t ad = acc_s + q2.j * ES;
+                    sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, q2.v, p)));
+                    if constexpr (KL) sts(cnt_s + q2.j * ES, add_rn(lds(cnt_s + q2.j * ES, T(0)), T(1)));
+                  }
+                }
+                __syncwarp();
+              }
             }
           }
         }
@@ -343,16 +363,19 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
 template <typename T, int KPL>
 __global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __restrict__ ci,
                                    const int32_t* __restrict__ order, const int64_t* __restrict__ item_off,
-                                   int64_t m, int k, int tile_major, int64_t n_tiles, int64_t base,
+                                   int64_t m, int k, int tile_major, int64_t n_tiles, int64_t n_bands,
+                                   int64_t base,
                                    T* __restrict__ od, int64_t* __restrict__ oi) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t band_items = item_off[m];
   for (int64_t p = warp; p < m; p += nw) {
     WarpTopK<T, KPL> top;
     top.init();
-    const int64_t n_lists = tile_major ? n_tiles : item_off[p + 1] - item_off[p];
+    const int64_t per_band = item_off[p + 1] - item_off[p];
+    const int64_t n_lists = tile_major ? n_tiles : per_band * n_bands;
     for (int64_t l = 0; l < n_lists; ++l) {
-      const int64_t it = tile_major ? l * m + p : item_off[p] + l;
+      const int64_t it = tile_major ? l * m + p : (l / per_band) * band_items + item_off[p] + l % per_band;
       for (int q = 0; q < k; q += 32) {
         const int j = q + int(lane_id());
         const bool ok = j < k;
@@ -409,10 +432,14 @@ int launch_isect_metric(IsectArgs<T>& args, int W, cudaStream_t st) {
     const int blocks = int(std::min<int64_t>((a.m * 32 + 255) / 256, int64_t(num_sms()) * 16));    \
     if (a.topk <= 32)                                                                               \
       merge_items_kernel<T, 1><<<blocks, 256, 0, st>>>(a.cand_d, a.cand_i, a.order, a.item_off,    \
-                                                        a.m, a.topk, a.tile_major, a.n_tiles, base, od, oi); \
+                                                        a.m, a.topk, a.tile_major, a.n_tiles,              \
+                                                        (a.n_tiles + a.band - 1) / a.band,                \
+                                                        base, od, oi);                                     \
     else                                                                                            \
       merge_items_kernel<T, 4><<<blocks, 256, 0, st>>>(a.cand_d, a.cand_i, a.order, a.item_off,    \
-                                                        a.m, a.topk, a.tile_major, a.n_tiles, base, od, oi); \
+                                                        a.m, a.topk, a.tile_major, a.n_tiles,              \
+                                                        (a.n_tiles + a.band - 1) / a.band,                \
+                                                        base, od, oi);                                     \
     SD_LAUNCH_CHECK();                                                                              \
     return SD_OK;                                                                                   \
   }
