@@ -15,7 +15,8 @@ import numpy as np
 
 from .errors import DimensionMismatch, DomainError, KTooLarge
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsemidist_b200.so")
+LIB_PATH = os.environ.get("SD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "libsemidist_b200.so")
 
 # sd_status (include/semidist_b200.h)
 SD_OK, SD_E_DIM, SD_E_DOMAIN_NEG, SD_E_DOMAIN_RADICAND, SD_E_KL_UNCOVERED = 0, 1, 2, 3, 4

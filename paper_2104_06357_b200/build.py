@@ -40,16 +40,25 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False):
-    os.makedirs(os.path.join(CSRC, "build"), exist_ok=True)
+def build(verbose=False, force=False, variant=None, defines=()):
+    """Compile every source and link LIB.  ``variant``/``defines`` build a
+    tuning variant (libsemidist_b200_<variant>.so) with extra -D flags."""
+    global LIB
+    lib_path = LIB if variant is None else os.path.join(HERE, f"libsemidist_b200_{variant}.so")
+    obj_dir = os.path.join(CSRC, "build" if variant is None else f"build_{variant}")
+    return _build(verbose, force, lib_path, obj_dir, list(defines))
+
+
+def _build(verbose, force, lib_path, obj_dir, defines):
+    os.makedirs(obj_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "semidist_b200.h")]
 
     def compile_one(src):
         path = os.path.join(CSRC, src)
-        obj = _obj(src)
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
         if not force and not _stale(obj, [path] + hdrs):
             return obj
-        cmd = [NVCC, *FLAGS, "-c", path, "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", path, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,14 +70,17 @@ def build(verbose=False, force=False):
 
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:
         objs = list(pool.map(compile_one, SOURCES))
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB,
+    if force or _stale(lib_path, objs):
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib_path,
                "-lcudart"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
+    args = sys.argv[1:]
+    variant = next((a.split("=", 1)[1] for a in args if a.startswith("--variant=")), None)
+    defines = [a[2:] for a in args if a.startswith("-D")]
+    print(build(verbose="--verbose" in args, force="--force" in args, variant=variant, defines=defines))

@@ -49,7 +49,10 @@ struct IsectArgs {
 constexpr int ISECT_MAX_WARPS = 14;
 
 // columns whose first 32 postings are loaded before any is applied
-template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
+#ifndef SD_ISECT_U32
+#define SD_ISECT_U32 32
+#endif
+template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? SD_ISECT_U32 : 16; };
 
 // 4 consecutive values through 16-byte shared/global accesses
 template <typename T> struct V4;

@@ -297,3 +297,24 @@ def _gather_rows(m, rows):
         newptr.append(newptr[-1] + hi - lo)
     return sd.CsrMatrix(len(rows), m.n_cols, np.asarray(newptr, dtype=np.int64),
                         np.concatenate(parts_i), np.concatenate(parts_v))
+
+
+def test_sharded_knn_emulated_on_one_gpu():
+    """B sharded into 3 ranges processed one after another on the same GPU,
+    merged with sd_topk_merge: equals the single-shard kNN (NCCL
+    cannot place two ranks on one GPU, so shards are emulated)."""
+    import torch
+    from paper_2104_06357_b200.distributed import local_topk_padded, merge_candidates, shard_bounds
+    x = _host(sd.generate(sd.GenSpec(500, 400, "zipf", zipf_s=1.2, zipf_max_degree=120, seed=31)))
+    q = sd.slice_rows(x, 0, 60)
+    spec = sd.metric_registry("cosine")
+    for k in (7, 40):
+        ds, is_ = [], []
+        for lo, hi in shard_bounds(x.n_rows, 3):
+            d, i = local_topk_padded(sd.slice_rows(x, lo, hi), q, k, spec, index_base=lo, dtype=np.float64)
+            ds.append(d)
+            is_.append(i)
+        md, mi = merge_candidates(torch.stack(ds), torch.stack(is_), k)
+        base = sd.kneighbors(x, q, k, spec)
+        np.testing.assert_array_equal(mi.cpu().numpy(), base.indices)
+        np.testing.assert_array_equal(md.cpu().numpy(), base.distances)
