@@ -151,7 +151,7 @@ static int fused_run(const sd_csr* a, const sd_csr* b, const sd_index* index, in
   Stats sa, sb;
   const int ph_stats = is_namm(md->metric) ? PH_PASS2 : PH_NORMS;
   tm.begin(ph_stats);
-  int rc = isect_stats(a, b, dtype, md, sabuf, sbbuf, &sa, &sb, st);
+  int rc = isect_stats(a, b, ix, dtype, md, sabuf, sbbuf, &sa, &sb, st);
   tm.end(ph_stats);
   if (rc == SD_OK) {
     tm.begin(PH_PASS1);

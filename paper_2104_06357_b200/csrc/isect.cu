@@ -20,6 +20,8 @@
 // HBM traffic is the output write plus posting reads, which stay L2-resident
 // per tile (DESIGN.md §7 byte model).
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <cub/cub.cuh>
 #include "common.cuh"
 #include "metric.cuh"
@@ -28,6 +30,16 @@
 #include "isect_kernel.cuh"
 
 struct sd_index {
+  // per-row statistics of the index rows, computed once per (metric, p) and
+  // owned by the index (they are a property of B, like the postings)
+  struct StatEntry {
+    int metric;
+    double p;
+    void* buf;
+    sd::Stats stats;
+  };
+  std::mutex mu;
+  std::vector<StatEntry> stat_cache;
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
   int tile = 0;
   int64_t n_tiles = 0;
@@ -200,17 +212,32 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
 
 // Per-row statistics of both sides for the fused epilogue (norms for the
 // dot family, one-sided sums for NAMM metrics, degrees of A for KL).
-int isect_stats(const sd_csr* a, const sd_csr* b, int dtype, const sd_metric_desc* md, Scratch& sa_buf,
-                Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st) {
+int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtype, const sd_metric_desc* md,
+                Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st) {
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t ns = metric_stats_count(md->metric);
   if (ns == 0) return SD_OK;
   SD_TRY(sa_buf.alloc(es * ns * stats_stride(std::max<int64_t>(1, a->n_rows)), st));
   SD_TRY(metric_stats(a, dtype, md, true, sa_buf.ptr, sa, st));
-  if (md->metric != SD_M_KL) {
+  if (md->metric == SD_M_KL) return SD_OK;
+  sd_index* ix = const_cast<sd_index*>(ix_c);
+  if (ix == nullptr) {
     SD_TRY(sb_buf.alloc(es * ns * stats_stride(std::max<int64_t>(1, b->n_rows)), st));
-    SD_TRY(metric_stats(b, dtype, md, false, sb_buf.ptr, sb, st));
+    return metric_stats(b, dtype, md, false, sb_buf.ptr, sb, st);
   }
+  const double pk = is_namm(md->metric) ? md->p : 0.0;
+  std::lock_guard<std::mutex> lock(ix->mu);
+  for (auto& e : ix->stat_cache)
+    if (e.metric == md->metric && e.p == pk) { *sb = e.stats; return SD_OK; }
+  sd_index::StatEntry e{md->metric, pk, nullptr, Stats()};
+  if (cudaMalloc(&e.buf, es * ns * stats_stride(std::max<int64_t>(1, b->n_rows))) != cudaSuccess) {
+    set_error("cudaMalloc failed for index statistics");
+    return SD_E_CUDA;
+  }
+  const int rc = metric_stats(b, dtype, md, false, e.buf, &e.stats, st);
+  if (rc != SD_OK) { cudaFree(e.buf); return rc; }
+  ix->stat_cache.push_back(e);
+  *sb = e.stats;
   return SD_OK;
 }
 
@@ -284,6 +311,7 @@ int sd_index_free(sd_index* ix) {
   if (!ix) return SD_OK;
   if (ix->colptr) cudaFree(ix->colptr);
   if (ix->post) cudaFree(ix->post);
+  for (auto& e : ix->stat_cache) cudaFree(e.buf);
   delete ix;
   return SD_OK;
 }

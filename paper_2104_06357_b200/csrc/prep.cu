@@ -1,8 +1,7 @@
 // prep.cu — per-row statistics and element-wise preparation kernels.
 //
-// Row reductions run one warp per row and accumulate SEQUENTIALLY in
-// ascending column order (lane 0's running value, fed 32 elements at a time
-// through shuffles).  The fused intersection kernel (isect.cu) accumulates
+// Row reductions run one thread per row and accumulate SEQUENTIALLY in
+// ascending column order.  The fused intersection kernel (isect.cu) accumulates
 // its per-cell dot products in the same ascending order, so ||a||^2 and
 // <a,a> are bitwise equal and self-distances of the expanded metrics come
 // out exactly 0, as they do in the reference (hard part 4).
@@ -22,36 +21,39 @@ __device__ __forceinline__ T stat_term(T v, T p) {
   else return product<SR, T>(T(0), v, p);  // STAT_ONESIDED_B
 }
 
+// One thread per row, sequential ascending sum (the same association order as
+// the fused kernel's per-cell accumulation).  Rows are independent, so
+// power-law rows only cost their own length; loads are unrolled 8-deep.
 template <typename T, int KIND, int SR>
 __global__ void row_stat_kernel(const int64_t* __restrict__ ptr, const T* __restrict__ val,
                                 int64_t n_rows, T p, T* __restrict__ out) {
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = lane_id();
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
     const int64_t beg = ptr[r], end = ptr[r + 1];
     T s = T(0);
     if constexpr (KIND == SD_STAT_L0) {
       s = T(end - beg);
     } else {
-      for (int64_t base = beg; base < end; base += 32) {
-        const int64_t e = base + lane;
-        T t = e < end ? stat_term<T, KIND, SR>(val[e], p) : T(0);
-        const int cnt = int(tmin<int64_t>(32, end - base));
-        for (int k = 0; k < cnt; ++k) s = add_rn(s, __shfl_sync(0xffffffffu, t, k));
+      int64_t e = beg;
+      for (; e + 8 <= end; e += 8) {
+        T t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = stat_term<T, KIND, SR>(__ldg(val + e + u), p);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = add_rn(s, t[u]);
       }
+      for (; e < end; ++e) s = add_rn(s, stat_term<T, KIND, SR>(__ldg(val + e), p));
       if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
     }
-    if (lane == 0) out[r] = s;
+    out[r] = s;
   }
 }
 
 template <typename T, int KIND, int SR>
 static int launch_stat(const sd_csr* m, T p, void* out, cudaStream_t st) {
   if (m->n_rows == 0) return SD_OK;
-  int64_t warps = m->n_rows;
-  int blocks = int(tmin<int64_t>((warps * 32 + 255) / 256, int64_t(num_sms()) * 16));
-  row_stat_kernel<T, KIND, SR><<<blocks, 256, 0, st>>>(
+  int blocks = int(tmin<int64_t>((m->n_rows + 127) / 128, int64_t(num_sms()) * 32));
+  row_stat_kernel<T, KIND, SR><<<blocks, 128, 0, st>>>(
       m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out));
   SD_LAUNCH_CHECK();
   return SD_OK;

@@ -41,8 +41,8 @@ int expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd_me
 int metric_semiring(int metric);
 int default_tile(int dtype);
 int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream_t st);
-int isect_stats(const sd_csr* a, const sd_csr* b, int dtype, const sd_metric_desc* md, Scratch& sa_buf,
-                Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st);
+int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
+                Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st);
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
               void* out_d, int64_t* out_i, uint32_t* flags, cudaStream_t st);
