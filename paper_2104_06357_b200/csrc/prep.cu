@@ -21,19 +21,33 @@ __device__ __forceinline__ T stat_term(T v, T p) {
   else return product<SR, T>(T(0), v, p);  // STAT_ONESIDED_B
 }
 
-// One thread per row, sequential ascending sum (the same association order as
-// the fused kernel's per-cell accumulation).  Rows are independent, so
-// power-law rows only cost their own length; loads are unrolled 8-deep.
+// Sequential ascending sums (the association order of the fused kernel's
+// per-cell accumulation).  A warp owns 32 consecutive rows: short rows are
+// summed by their own lane; each long row (power-law tail) is then summed by
+// the whole warp — chunks of 256 values loaded coalesced (next chunk in flight
+// while the current one is summed), staged in shared memory and added in
+// order by lane 0 — so a 25k-entry row costs ~its FADD chain, not 25k
+// dependent global loads.
+constexpr int STAT_LONG = 64;
+constexpr int STAT_CHUNK = 256;
+constexpr int STAT_WARPS = 4;
+
 template <typename T, int KIND, int SR>
-__global__ void row_stat_kernel(const int64_t* __restrict__ ptr, const T* __restrict__ val,
-                                int64_t n_rows, T p, T* __restrict__ out) {
-  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
-       r += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t beg = ptr[r], end = ptr[r + 1];
+__global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t* __restrict__ ptr,
+                                                                   const T* __restrict__ val, int64_t n_rows,
+                                                                   T p, T* __restrict__ out) {
+  __shared__ T stage[STAT_WARPS][STAT_CHUNK];
+  const unsigned lane = lane_id();
+  const int w = threadIdx.x >> 5;
+  const int64_t nwarps = int64_t(gridDim.x) * STAT_WARPS;
+  for (int64_t r0 = (int64_t(blockIdx.x) * STAT_WARPS + w) * 32; r0 < n_rows; r0 += nwarps * 32) {
+    const int64_t r = r0 + lane;
+    const bool ok = r < n_rows;
+    const int64_t beg = ok ? ptr[r] : 0, end = ok ? ptr[r + 1] : 0;
     T s = T(0);
     if constexpr (KIND == SD_STAT_L0) {
       s = T(end - beg);
-    } else {
+    } else if (end - beg <= STAT_LONG) {
       int64_t e = beg;
       for (; e + 8 <= end; e += 8) {
         T t[8];
@@ -43,17 +57,50 @@ __global__ void row_stat_kernel(const int64_t* __restrict__ ptr, const T* __rest
         for (int u = 0; u < 8; ++u) s = add_rn(s, t[u]);
       }
       for (; e < end; ++e) s = add_rn(s, stat_term<T, KIND, SR>(__ldg(val + e), p));
+    }
+    if constexpr (KIND != SD_STAT_L0) {
+      unsigned long_mask = __ballot_sync(0xffffffffu, ok && end - beg > STAT_LONG);
+      while (long_mask) {
+        const int src = __ffs(long_mask) - 1;
+        long_mask &= long_mask - 1;
+        const int64_t lb = __shfl_sync(0xffffffffu, beg, src), le = __shfl_sync(0xffffffffu, end, src);
+        T ls = T(0);
+        T nxt[STAT_CHUNK / 32];
+#pragma unroll
+        for (int k = 0; k < STAT_CHUNK / 32; ++k) {
+          const int64_t e = lb + k * 32 + lane;
+          nxt[k] = e < le ? __ldg(val + e) : T(0);
+        }
+        for (int64_t c = lb; c < le; c += STAT_CHUNK) {
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < STAT_CHUNK / 32; ++k) stage[w][k * 32 + lane] = nxt[k];
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < STAT_CHUNK / 32; ++k) {  // next chunk in flight during the serial sum
+            const int64_t e = c + STAT_CHUNK + k * 32 + lane;
+            nxt[k] = e < le ? __ldg(val + e) : T(0);
+          }
+          if (lane == 0) {
+            const int cnt = int(tmin<int64_t>(STAT_CHUNK, le - c));
+            for (int q = 0; q < cnt; ++q) ls = add_rn(ls, stat_term<T, KIND, SR>(stage[w][q], p));
+          }
+        }
+        ls = __shfl_sync(0xffffffffu, ls, 0);
+        if (int(lane) == src) s = ls;
+      }
       if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
     }
-    out[r] = s;
+    if (ok) out[r] = s;
   }
 }
 
 template <typename T, int KIND, int SR>
 static int launch_stat(const sd_csr* m, T p, void* out, cudaStream_t st) {
   if (m->n_rows == 0) return SD_OK;
-  int blocks = int(tmin<int64_t>((m->n_rows + 127) / 128, int64_t(num_sms()) * 32));
-  row_stat_kernel<T, KIND, SR><<<blocks, 128, 0, st>>>(
+  const int64_t warps = (m->n_rows + 31) / 32;
+  int blocks = int(tmin<int64_t>((warps + STAT_WARPS - 1) / STAT_WARPS, int64_t(num_sms()) * 16));
+  row_stat_kernel<T, KIND, SR><<<blocks, STAT_WARPS * 32, 0, st>>>(
       m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out));
   SD_LAUNCH_CHECK();
   return SD_OK;
