@@ -224,7 +224,9 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
     fused = strategy is None or (isinstance(strategy, str) and strategy == "auto")
     report = _engine_report(da, db, passes, name, strategy, a, b)
     host_out = out
-    ldo = (b.n_rows + 3) // 4 * 4   # 16-byte aligned rows let the kernel store 4 cells per lane
+    # 16-byte aligned rows let the kernel store 4 cells per lane; a host `out`
+    # is filled by one contiguous D2H copy, so it gets an unpadded buffer
+    ldo = b.n_rows if out is not None else (b.n_rows + 3) // 4 * 4
     out_buf = torch.empty((a.n_rows, ldo), dtype=tdt, device=da.device)
     out = out_buf[:, :b.n_rows]
     flags = _lib.new_flags(da.device)
