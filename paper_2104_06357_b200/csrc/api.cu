@@ -257,7 +257,7 @@ int sd_expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd
               const void* const* stats_a, const void* const* stats_b, uint32_t* dev_flags, sd_stream_t stream) {
   SD_TRY(check_metric(md));
   Stats sa, sb;
-  const int64_t ns = metric_stats_count(md->metric);
+  const int64_t ns = metric_expand_stats_count(md->metric);
   if (!is_namm(md->metric) && md->metric != SD_M_KL) {
     for (int64_t q = 0; q < ns; ++q) {
       sa.s[q] = stats_a ? stats_a[q] : nullptr;

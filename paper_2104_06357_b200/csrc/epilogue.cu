@@ -26,10 +26,15 @@ bool metric_two_pass(int metric) { return is_namm(metric); }
 // number of per-row statistic arrays the epilogue reads for a metric
 int64_t metric_stats_count(int metric) {
   switch (metric) {
-    case SD_M_CORRELATION: return 2;
-    case SD_M_COSINE: case SD_M_DICE: case SD_M_EUCLIDEAN: case SD_M_JACCARD: case SD_M_KL: return 1;
+    case SD_M_CORRELATION: case SD_M_COSINE: return 2;
+    case SD_M_DICE: case SD_M_EUCLIDEAN: case SD_M_JACCARD: case SD_M_KL: return 1;
     default: return is_namm(metric) ? 1 : 0;
   }
+}
+
+// statistics the element-wise expansion (sd_expand) reads
+int64_t metric_expand_stats_count(int metric) {
+  return metric == SD_M_COSINE ? 1 : metric_stats_count(metric);
 }
 
 // Fill `buf` (n_rows * metric_stats_count values) with the statistics
@@ -48,9 +53,10 @@ int metric_stats(const sd_csr* m, int dtype, const sd_metric_desc* md, bool a_si
       SD_TRY(row_stat(m, dtype, SD_STAT_L2SQ, 0, 0.0, slot(1), st));
       out->s[0] = slot(0); out->s[1] = slot(1);
       return SD_OK;
-    case SD_M_COSINE:
+    case SD_M_COSINE:  // s1 = 1/l2 for the fused epilogue
       SD_TRY(row_stat(m, dtype, SD_STAT_L2, 0, 0.0, slot(0), st));
-      out->s[0] = slot(0);
+      SD_TRY(row_stat(m, dtype, STAT_INV_L2, 0, 0.0, slot(1), st));
+      out->s[0] = slot(0); out->s[1] = slot(1);
       return SD_OK;
     case SD_M_DICE: case SD_M_JACCARD: case SD_M_KL:
       SD_TRY(row_stat(m, dtype, SD_STAT_L0, 0, 0.0, slot(0), st));

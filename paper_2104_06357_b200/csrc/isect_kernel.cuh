@@ -136,8 +136,8 @@ __device__ __forceinline__ void sts4_zero(uint32_t a, double) {
 // sparse data): the epilogue then skips the division entirely.
 template <int M>
 __host__ __device__ constexpr bool sparse_result() {
-  return M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_JACCARD || M == SD_M_DOT ||
-         M == SD_M_RUSSELRAO || M == SD_M_HELLINGER;
+  return M == SD_M_DICE || M == SD_M_JACCARD || M == SD_M_DOT || M == SD_M_RUSSELRAO ||
+         M == SD_M_HELLINGER;
 }
 
 template <typename T, int M>
@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
   constexpr bool KL = CK == C_KL;
   constexpr bool SB0 = (M == SD_M_CORRELATION || M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_EUCLIDEAN ||
                         M == SD_M_JACCARD || is_namm(M));
-  constexpr bool SB1 = M == SD_M_CORRELATION;
+  constexpr bool SB1 = M == SD_M_CORRELATION || M == SD_M_COSINE;
+  // cosine: branch-free 1 - d * (1/||a||) * (1/||b||) (reciprocals from row_stat)
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int U = IsectU<T>::value;
   const int warp = threadIdx.x >> 5;
@@ -251,13 +252,24 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
         av = valid ? a.a_val[e] : T(0);
         for (int q0 = 0; q0 < ncol; q0 += U) {
           Posting<T> ps[U];
+          if (ncol == 32) {  // full batch: no per-column bounds test
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
-            const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
-            const uint32_t pp = b0 + lane;
-            ps[u].j = 0xffffffffu;
-            if (q0 + u < ncol && pp < b1) ps[u] = load_posting(post + pp);
+            for (int u = 0; u < U; ++u) {
+              const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
+              const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
+              const uint32_t pp = b0 + lane;
+              ps[u].j = 0xffffffffu;
+              if (pp < b1) ps[u] = load_posting(post + pp);
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
+              const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
+              const uint32_t pp = b0 + lane;
+              ps[u].j = 0xffffffffu;
+              if (q0 + u < ncol && pp < b1) ps[u] = load_posting(post + pp);
+            }
           }
           if (q0 + U >= ncol) {  // last group of this batch: start the next batch's colptr loads
             pb = valid ? cp[c] : 0u;
@@ -330,6 +342,16 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
           }
         }
         T r[4];
+        if constexpr (M == SD_M_COSINE) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (ra0 > T(0)) {
+              r[u] = sub_rn(T(1), mul_rn(v[u], mul_rn(ra1, b1[u])));   // b1 = 1/||b|| (0 if empty)
+            } else {  // empty query row (metrics.py:116-118): 0 against empty rows, else 1
+              r[u] = b0[u] == T(0) ? T(0) : T(1);
+            }
+          }
+        } else
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (fast_zero && v[u] == T(0)) {

@@ -15,7 +15,7 @@ template <typename T, int KIND, int SR>
 __device__ __forceinline__ T stat_term(T v, T p) {
   if constexpr (KIND == SD_STAT_L0) return T(1);
   else if constexpr (KIND == SD_STAT_L1) return abs_(v);
-  else if constexpr (KIND == SD_STAT_L2 || KIND == SD_STAT_L2SQ) return mul_rn(v, v);
+  else if constexpr (KIND == SD_STAT_L2 || KIND == SD_STAT_L2SQ || KIND == STAT_INV_L2) return mul_rn(v, v);
   else if constexpr (KIND == SD_STAT_SUM) return v;
   else if constexpr (KIND == STAT_ONESIDED_A) return product<SR, T>(v, T(0), p);
   else return product<SR, T>(T(0), v, p);  // STAT_ONESIDED_B
@@ -90,6 +90,10 @@ __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t
         if (int(lane) == src) s = ls;
       }
       if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
+      if constexpr (KIND == STAT_INV_L2) {
+        s = sqrt_rn(s);
+        s = s > T(0) ? div_rn(T(1), s) : T(0);
+      }
     }
     if (ok) out[r] = s;
   }
@@ -116,6 +120,7 @@ int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void*
       case SD_STAT_L2: return launch_stat<T, SD_STAT_L2, 0>(m, pp, out, st);
       case SD_STAT_L2SQ: return launch_stat<T, SD_STAT_L2SQ, 0>(m, pp, out, st);
       case SD_STAT_SUM: return launch_stat<T, SD_STAT_SUM, 0>(m, pp, out, st);
+      case STAT_INV_L2: return launch_stat<T, STAT_INV_L2, 0>(m, pp, out, st);
       case STAT_ONESIDED_A:
         return SD_DISPATCH_SEMIRING(semiring, SR, [&]() -> int { return launch_stat<T, STAT_ONESIDED_A, SR>(m, pp, out, st); });
       case STAT_ONESIDED_B:

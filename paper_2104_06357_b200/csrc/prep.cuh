@@ -15,6 +15,8 @@ struct Stats {  // per-row statistics the metric epilogue reads (metric.cuh layo
 //   S_A[i] = sum_c ⊗(a_ic, 0)   and   S_B[j] = sum_c ⊗(0, b_jc)
 constexpr int STAT_ONESIDED_A = 16;
 constexpr int STAT_ONESIDED_B = 17;
+// 1/||row||_2 (0 for an empty row): the fused cosine epilogue multiplies instead of dividing
+constexpr int STAT_INV_L2 = 18;
 
 int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void* out,
              cudaStream_t st);
@@ -34,6 +36,7 @@ void reference_report(const int64_t* degrees, int64_t n_rows, const sd_strategy*
 int metric_stats(const sd_csr* m, int dtype, const sd_metric_desc* md, bool a_side, void* buf,
                  Stats* out, cudaStream_t st);
 int64_t metric_stats_count(int metric);
+int64_t metric_expand_stats_count(int metric);
 int expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd_metric_desc* md,
            int64_t n_cols, const Stats& sa, const Stats& sb, const void* miss,
            uint32_t* flags, cudaStream_t st);
