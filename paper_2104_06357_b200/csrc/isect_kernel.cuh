@@ -228,17 +228,24 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
     if constexpr (KPL > 0) top.init();
 
+    // the first 32 columns of the query and their posting ranges in tile t0;
+    // later tiles get theirs prefetched during the previous tile's epilogue
+    const bool valid0 = abeg + lane < aend;
+    const int32_t c0 = valid0 ? a.a_idx[abeg + lane] : 0;
+    const T av0 = valid0 ? a.a_val[abeg + lane] : T(0);
+    uint32_t pb0 = valid0 ? a.colptr[t0 * a.n_cols + c0] : 0u;
+    uint32_t pe0 = valid0 ? a.colptr[t0 * a.n_cols + c0 + 1] : 0u;
     for (int64_t t = t0; t < t1; ++t) {
       const int64_t j0 = t * TJ;
       const int nt = int(tmin<int64_t>(TJ, a.n - j0));
       const uint32_t* cp = a.colptr + t * a.n_cols;
       // software pipeline: (column, value, posting range) of the next 32 columns
       int64_t e = abeg + lane;
-      bool valid = e < aend;
-      int32_t c = valid ? a.a_idx[e] : 0;
-      T av = valid ? a.a_val[e] : T(0);
-      uint32_t pb = valid ? cp[c] : 0u;
-      uint32_t pe = valid ? cp[c + 1] : 0u;
+      bool valid = valid0;
+      int32_t c = c0;
+      T av = av0;
+      uint32_t pb = pb0;
+      uint32_t pe = pe0;
       for (int64_t base = abeg; base < aend; base += 32) {
         const int ncol = int(tmin<int64_t>(32, aend - base));
         const uint32_t cur_pb = pb;
@@ -315,32 +322,45 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
           }
         }
       }
+      if (t + 1 < t1) {  // next tile's first-batch posting ranges, in flight during the epilogue
+        pb0 = valid0 ? cp[a.n_cols + c0] : 0u;
+        pe0 = valid0 ? cp[a.n_cols + c0 + 1] : 0u;
+      }
       // epilogue: each lane finishes 4 consecutive cells per step (16-byte
       // shared/global accesses); the accumulator is re-zeroed as it is read
       T* orow = KPL == 0 ? a.out + i * a.ldo + j0 : nullptr;
-      for (int qb = 0; qb < nt; qb += 128) {  // warp-uniform trip count (top-k offers are collective)
+      // group g (128 cells) is computed while group g+1's shared and global
+      // loads are in flight (the statistic load is an L2 round trip)
+      T v[4], cv[4], b0[4], b1[4];
+      auto load_group = [&](int qb, T* gv, T* gcv, T* gb0, T* gb1) {
         const int q = qb + 4 * lane;
-        const bool full = q + 3 < nt;
-        T v[4] = {T(0), T(0), T(0), T(0)}, cv[4] = {T(0), T(0), T(0), T(0)};
-        T b0[4] = {T(0), T(0), T(0), T(0)}, b1[4] = {T(0), T(0), T(0), T(0)};
-        if (full) {
-          lds4(acc_s + q * ES, v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { gv[u] = T(0); gcv[u] = T(0); gb0[u] = T(0); gb1[u] = T(0); }
+        if (q + 3 < nt) {
+          lds4(acc_s + q * ES, gv);
           sts4_zero(acc_s + q * ES, T(0));
-          if constexpr (KL) { lds4(cnt_s + q * ES, cv); sts4_zero(cnt_s + q * ES, T(0)); }
-          if constexpr (SB0) V4<T>::load(a.sb0 + j0 + q, b0);
-          if constexpr (SB1) V4<T>::load(a.sb1 + j0 + q, b1);
+          if constexpr (KL) { lds4(cnt_s + q * ES, gcv); sts4_zero(cnt_s + q * ES, T(0)); }
+          if constexpr (SB0) V4<T>::load(a.sb0 + j0 + q, gb0);
+          if constexpr (SB1) V4<T>::load(a.sb1 + j0 + q, gb1);
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (q + u < nt) {
-              v[u] = lds(acc_s + (q + u) * ES, T(0));
+              gv[u] = lds(acc_s + (q + u) * ES, T(0));
               sts(acc_s + (q + u) * ES, T(0));
-              if constexpr (KL) { cv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
-              if constexpr (SB0) b0[u] = a.sb0[j0 + q + u];
-              if constexpr (SB1) b1[u] = a.sb1[j0 + q + u];
+              if constexpr (KL) { gcv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
+              if constexpr (SB0) gb0[u] = a.sb0[j0 + q + u];
+              if constexpr (SB1) gb1[u] = a.sb1[j0 + q + u];
             }
           }
         }
+      };
+      load_group(0, v, cv, b0, b1);
+      for (int qb = 0; qb < nt; qb += 128) {  // warp-uniform trip count (top-k offers are collective)
+        const int q = qb + 4 * lane;
+        const bool full = q + 3 < nt;
+        T nv[4], ncv[4], nb0[4], nb1[4];
+        if (qb + 128 < nt) load_group(qb + 128, nv, ncv, nb0, nb1);
         T r[4];
         if constexpr (M == SD_M_COSINE) {
 #pragma unroll
@@ -374,6 +394,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               if (q + u < nt) orow[q + u] = r[u];
           }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { v[u] = nv[u]; cv[u] = ncv[u]; b0[u] = nb0[u]; b1[u] = nb1[u]; }
       }
       __syncwarp();
     }
