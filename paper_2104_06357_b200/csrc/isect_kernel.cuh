@@ -355,31 +355,29 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
           }
         }
       };
-      load_group(0, v, cv, b0, b1);
-      for (int qb = 0; qb < nt; qb += 128) {  // warp-uniform trip count (top-k offers are collective)
+      auto finish_group = [&](int qb, const T* gv, const T* gcv, const T* gb0, const T* gb1) {
         const int q = qb + 4 * lane;
         const bool full = q + 3 < nt;
-        T nv[4], ncv[4], nb0[4], nb1[4];
-        if (qb + 128 < nt) load_group(qb + 128, nv, ncv, nb0, nb1);
         T r[4];
         if constexpr (M == SD_M_COSINE) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (ra0 > T(0)) {
-              r[u] = sub_rn(T(1), mul_rn(v[u], mul_rn(ra1, b1[u])));   // b1 = 1/||b|| (0 if empty)
+              r[u] = sub_rn(T(1), mul_rn(gv[u], mul_rn(ra1, gb1[u])));   // gb1 = 1/||b|| (0 if empty)
             } else {  // empty query row (metrics.py:116-118): 0 against empty rows, else 1
-              r[u] = b0[u] == T(0) ? T(0) : T(1);
+              r[u] = gb0[u] == T(0) ? T(0) : T(1);
             }
           }
-        } else
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (fast_zero && v[u] == T(0)) {
-            r[u] = zero_val;
-          } else {
-            uint32_t f = 0;
-            r[u] = fused_value<T, M>(a, v[u], cv[u], ra0, ra1, b0[u], b1[u], f);
-            if (q + u < nt) flags |= f;  // lanes past the tile end evaluate a dummy cell
+          for (int u = 0; u < 4; ++u) {
+            if (fast_zero && gv[u] == T(0)) {
+              r[u] = zero_val;
+            } else {
+              uint32_t f = 0;
+              r[u] = fused_value<T, M>(a, gv[u], gcv[u], ra0, ra1, gb0[u], gb1[u], f);
+              if (q + u < nt) flags |= f;  // lanes past the tile end evaluate a dummy cell
+            }
           }
         }
         if constexpr (KPL > 0) {
@@ -394,8 +392,18 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               if (q + u < nt) orow[q + u] = r[u];
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { v[u] = nv[u]; cv[u] = ncv[u]; b0[u] = nb0[u]; b1[u] = nb1[u]; }
+      };
+      // ping-pong: finish group g from one register set while group g+1 loads
+      // into the other (no copies, so the loads stay in flight)
+      T v2[4], cv2[4], b02[4], b12[4];
+      load_group(0, v, cv, b0, b1);
+      for (int qb = 0; qb < nt; qb += 256) {  // warp-uniform trip count (top-k offers are collective)
+        if (qb + 128 < nt) load_group(qb + 128, v2, cv2, b02, b12);
+        finish_group(qb, v, cv, b0, b1);
+        if (qb + 128 < nt) {
+          if (qb + 256 < nt) load_group(qb + 256, v, cv, b0, b1);
+          finish_group(qb + 128, v2, cv2, b02, b12);
+        }
       }
       __syncwarp();
     }
