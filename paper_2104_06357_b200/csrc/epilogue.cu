@@ -54,8 +54,7 @@ int metric_stats(const sd_csr* m, int dtype, const sd_metric_desc* md, bool a_si
       out->s[0] = slot(0); out->s[1] = slot(1);
       return SD_OK;
     case SD_M_COSINE:  // s1 = 1/l2 for the fused epilogue
-      SD_TRY(row_stat(m, dtype, SD_STAT_L2, 0, 0.0, slot(0), st));
-      SD_TRY(row_stat(m, dtype, STAT_INV_L2, 0, 0.0, slot(1), st));
+      SD_TRY(row_stat_l2_inv(m, dtype, slot(0), slot(1), st));
       out->s[0] = slot(0); out->s[1] = slot(1);
       return SD_OK;
     case SD_M_DICE: case SD_M_JACCARD: case SD_M_KL:

@@ -46,6 +46,8 @@ struct sd_index {
   int dtype = 0;
   uint32_t* colptr = nullptr;  // [n_tiles * n_cols + 1]
   void* post = nullptr;        // [nnz] Posting<T> (row id within tile, value)
+  uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
+  void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
   int64_t bytes = 0;
 };
 
@@ -73,7 +75,8 @@ template <typename T>
 __global__ void index_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                      const T* __restrict__ val, int64_t n_rows, int tile, int64_t n_cols,
                                      const uint32_t* __restrict__ colptr, uint32_t* cursor,
-                                     Posting<T>* __restrict__ post) {
+                                     Posting<T>* __restrict__ post, const uint8_t* __restrict__ rank,
+                                     uint8_t* __restrict__ post_rank) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = warp; r < n_rows; r += nw) {
@@ -87,6 +90,7 @@ __global__ void index_scatter_kernel(const int64_t* __restrict__ ptr, const int3
       q.v = val[e];
       if constexpr (sizeof(T) == 8) q.pad = 0;
       post[pos] = q;
+      post_rank[pos] = rank[e];
     }
   }
 }
@@ -104,11 +108,13 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
   auto fail = [&](int code) { sd_index_free(ix); return code; };
   const size_t ps = dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>);
   if (cudaMalloc(&ix->colptr, sizeof(uint32_t) * (n_keys + 1)) != cudaSuccess ||
-      cudaMalloc(&ix->post, ps * std::max<int64_t>(1, b->nnz)) != cudaSuccess) {
+      cudaMalloc(&ix->post, ps * std::max<int64_t>(1, b->nnz)) != cudaSuccess ||
+      cudaMalloc(&ix->post_rank, std::max<int64_t>(1, b->nnz)) != cudaSuccess ||
+      cudaMalloc(&ix->topb, es * CHEB_K * std::max<int64_t>(1, b->n_rows)) != cudaSuccess) {
     set_error("cudaMalloc failed for the inverted index");
     return fail(SD_E_CUDA);
   }
-  ix->bytes = int64_t(sizeof(uint32_t) * (n_keys + 1) + ps * b->nnz);
+  ix->bytes = int64_t(sizeof(uint32_t) * (n_keys + 1) + (ps + 1) * b->nnz + es * CHEB_K * b->n_rows);
   Scratch counts;
   if (counts.alloc(sizeof(uint32_t) * (n_keys + 1), st) != SD_OK) return fail(SD_E_CUDA);
   if (cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (n_keys + 1), st) != cudaSuccess) return fail(SD_E_CUDA);
@@ -126,11 +132,15 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
     return fail(SD_E_CUDA);
   }
   if (cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (n_keys + 1), st) != cudaSuccess) return fail(SD_E_CUDA);
+  Scratch rank;
+  if (rank.alloc(std::max<int64_t>(1, b->nnz), st) != SD_OK) return fail(SD_E_CUDA);
+  if (row_topk(b, dtype, rank.as<uint8_t>(), ix->topb, st) != SD_OK) return fail(SD_E_CUDA);
   if (b->n_rows > 0 && b->nnz > 0) {
     int rc = SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
       index_scatter_kernel<T><<<blocks, 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
                                                       b->n_rows, tile, b->n_cols, ix->colptr,
-                                                      counts.as<uint32_t>(), static_cast<Posting<T>*>(ix->post));
+                                                      counts.as<uint32_t>(), static_cast<Posting<T>*>(ix->post),
+                                                      rank.as<uint8_t>(), ix->post_rank);
       SD_LAUNCH_CHECK();
       return SD_OK;
     });
@@ -215,6 +225,20 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
 int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtype, const sd_metric_desc* md,
                 Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st) {
   const size_t es = dtype == SD_F64 ? 8 : 4;
+  if (md->metric == SD_M_CHEBYSHEV) {  // top-K |a| per query row + per-entry ranks; B side lives in the index
+    const int64_t stride = stats_stride(std::max<int64_t>(1, a->n_rows));
+    const int64_t nnz_span = std::max<int64_t>(1, a->nnz);
+    SD_TRY(sa_buf.alloc(es * CHEB_K * stride + nnz_span, st));
+    uint8_t* rank = reinterpret_cast<uint8_t*>(static_cast<char*>(sa_buf.ptr) + es * CHEB_K * stride);
+    // top values K-major with row stride `stride`: row_topk writes [r * n_rows + row]
+    sd_csr a2 = *a;
+    SD_TRY(row_topk(&a2, dtype, rank, sa_buf.ptr, st));
+    sa->s[0] = sa_buf.ptr;
+    sa->s[2] = rank;
+    if (!ix_c) { set_error("chebyshev fused path needs the index"); return SD_E_INVALID; }
+    sb->s[0] = ix_c->topb;
+    return SD_OK;
+  }
   const int64_t ns = metric_stats_count(md->metric);
   if (ns == 0) return SD_OK;
   SD_TRY(sa_buf.alloc(es * ns * stats_stride(std::max<int64_t>(1, a->n_rows)), st));
@@ -255,7 +279,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   if (m == 0 || b->n_rows == 0) return SD_OK;
   if (m >= (int64_t(1) << 31)) { set_error("too many query rows"); return SD_E_INVALID; }
   const size_t es = dtype == SD_F64 ? 8 : 4;
-  const int64_t per_warp = int64_t(ix->tile) * int64_t(es) * (ck == C_KL ? 2 : 1);
+  const int64_t per_warp = int64_t(ix->tile) * int64_t(es) * ((ck == C_KL || ck == C_MAX) ? 2 : 1);
   const int W = int(std::min<int64_t>(ISECT_MAX_WARPS, (smem_optin_bytes() - 2048) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const int64_t warps = int64_t(num_sms()) * W;
@@ -299,6 +323,11 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.out = static_cast<T*>(out); args.ldo = ldo; args.flags = flags;
     args.topk = topk;
     args.cand_d = cand_d.as<T>(); args.cand_i = cand_i.as<int64_t>();
+    args.a_rank = static_cast<const uint8_t*>(sa.s[2]);
+    args.post_rank = ix->post_rank;
+    args.topa = static_cast<const T*>(sa.s[0]);
+    args.topb = static_cast<const T*>(ix->topb);
+    args.b_ptr = b->indptr; args.b_idx = b->indices; args.b_val = static_cast<const T*>(b->values);
     SD_TRY(isect_launch(args, md->metric, W, st));
     if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
     return SD_OK;
@@ -311,6 +340,8 @@ int sd_index_free(sd_index* ix) {
   if (!ix) return SD_OK;
   if (ix->colptr) cudaFree(ix->colptr);
   if (ix->post) cudaFree(ix->post);
+  if (ix->post_rank) cudaFree(ix->post_rank);
+  if (ix->topb) cudaFree(ix->topb);
   for (auto& e : ix->stat_cache) cudaFree(e.buf);
   delete ix;
   return SD_OK;

@@ -42,7 +42,21 @@ struct IsectArgs {
   int topk;
   T* cand_d;                // kNN: per-item candidate lists [items][topk]
   int64_t* cand_i;
+  // fused chebyshev (C_MAX)
+  const uint8_t* a_rank;    // rank of each A entry in its row (top-CHEB_K by |a|, else 255)
+  const uint8_t* post_rank; // rank of each posting's value in its B row
+  const T* topa;            // [CHEB_K][m] largest |a| per query row
+  const T* topb;            // [CHEB_K][n] largest |b| per index row
+  const int64_t* b_ptr;     // index CSR, for the exact fallback of a fully-hit top-K
+  const int32_t* b_idx;
+  const T* b_val;
 };
+
+// chebyshev hit masks live in the second accumulator array as raw bits
+__device__ __forceinline__ uint32_t to_mask(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ uint32_t to_mask(double v) { return uint32_t(v); }
+__device__ __forceinline__ float from_mask(uint32_t m, float) { return __uint_as_float(m); }
+__device__ __forceinline__ double from_mask(uint32_t m, double) { return double(m); }
 
 // warps per CTA (one CTA per SM: 14 x 16 KB accumulators = 224 KB); capping
 // the CTA at 448 threads gives each thread up to 144 registers
@@ -163,7 +177,8 @@ template <typename T, int M, int KPL>
 __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const IsectArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CK = metric_contrib(M);
-  constexpr bool KL = CK == C_KL;
+  constexpr bool MX = CK == C_MAX;
+  constexpr bool KL = CK == C_KL || MX;   // second per-cell array: KL counts / chebyshev masks
   constexpr bool SB0 = (M == SD_M_CORRELATION || M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_EUCLIDEAN ||
                         M == SD_M_JACCARD || is_namm(M));
   constexpr bool SB1 = M == SD_M_CORRELATION || M == SD_M_COSINE;
@@ -186,6 +201,27 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
   const int64_t total_items = a.tile_major ? band_items : band_items * ((a.n_tiles + a.band - 1) / a.band);
   const bool vec_out = KPL == 0 && (a.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
   uint32_t flags = 0;
+
+  // one posting (row jr, value bv) of a column with query value x (and, for
+  // chebyshev, query-entry rank xr; jr then carries the posting's rank in bits 16..23)
+  auto apply_posting = [&](uint32_t jr, T bv, T x, uint32_t xr) {
+    if constexpr (MX) {
+      const uint32_t jl = jr & 0xffffu, rb = jr >> 16;
+      const uint32_t ad = acc_s + jl * ES;
+      const T m = contrib<CK, T>(x, bv, p);
+      const T old = lds(ad, T(0));
+      sts(ad, m > old ? m : old);
+      const uint32_t bits = (xr < CHEB_K ? (1u << xr) : 0u) | (rb < CHEB_K ? (1u << (16 + rb)) : 0u);
+      if (bits) {
+        const uint32_t am = cnt_s + jl * ES;
+        sts(am, from_mask(to_mask(lds(am, T(0))) | bits, T(0)));
+      }
+    } else {
+      const uint32_t ad = acc_s + jr * ES;
+      sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, bv, p)));
+      if constexpr (KL) sts(cnt_s + jr * ES, add_rn(lds(cnt_s + jr * ES, T(0)), T(1)));
+    }
+  };
 
   for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
     sts(acc_s + q * ES, T(0));
@@ -217,6 +253,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
     const T ra0 = a.sa0 ? a.sa0[i] : T(0);
     const T ra1 = a.sa1 ? a.sa1[i] : T(0);
+    T topa_l = T(0);  // chebyshev: lane r holds the r-th largest |a| of the query row
+    if constexpr (MX) topa_l = lane < CHEB_K ? a.topa[int64_t(lane) * a.m + i] : T(0);
     // value of a cell without intersections when the query row is non-empty
     bool fast_zero = false;
     T zero_val = T(0);
@@ -233,6 +271,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
     const bool valid0 = abeg + lane < aend;
     const int32_t c0 = valid0 ? a.a_idx[abeg + lane] : 0;
     const T av0 = valid0 ? a.a_val[abeg + lane] : T(0);
+    const uint32_t ar0 = (MX && valid0) ? a.a_rank[abeg + lane] : 255u;
     uint32_t pb0 = valid0 ? a.colptr[t0 * a.n_cols + c0] : 0u;
     uint32_t pe0 = valid0 ? a.colptr[t0 * a.n_cols + c0 + 1] : 0u;
     for (int64_t t = t0; t < t1; ++t) {
@@ -244,12 +283,14 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
       bool valid = valid0;
       int32_t c = c0;
       T av = av0;
+      uint32_t ar = ar0;
       uint32_t pb = pb0;
       uint32_t pe = pe0;
       for (int64_t base = abeg; base < aend; base += 32) {
         const int ncol = int(tmin<int64_t>(32, aend - base));
         const uint32_t cur_pb = pb;
         const T cur_av = av;
+        const uint32_t cur_ar = ar;
         const unsigned long_mask = __ballot_sync(FULL, pe - pb > 32u);
         const uint32_t cur_pe = pe;
         // next batch's columns (independent of this batch's postings)
@@ -257,6 +298,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
         valid = e < aend;
         c = valid ? a.a_idx[e] : 0;
         av = valid ? a.a_val[e] : T(0);
+        if constexpr (MX) ar = valid ? a.a_rank[e] : 255u;
         for (int q0 = 0; q0 < ncol; q0 += U) {
           Posting<T> ps[U];
           if (ncol == 32) {  // full batch: no per-column bounds test
@@ -266,7 +308,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
               const uint32_t pp = b0 + lane;
               ps[u].j = 0xffffffffu;
-              if (pp < b1) ps[u] = load_posting(post + pp);
+              if (pp < b1) {
+                ps[u] = load_posting(post + pp);
+                if constexpr (MX) ps[u].j |= uint32_t(a.post_rank[pp]) << 16;
+              }
             }
           } else {
 #pragma unroll
@@ -275,7 +320,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
               const uint32_t pp = b0 + lane;
               ps[u].j = 0xffffffffu;
-              if (q0 + u < ncol && pp < b1) ps[u] = load_posting(post + pp);
+              if (q0 + u < ncol && pp < b1) {
+                ps[u] = load_posting(post + pp);
+                if constexpr (MX) ps[u].j |= uint32_t(a.post_rank[pp]) << 16;
+              }
             }
           }
           if (q0 + U >= ncol) {  // last group of this batch: start the next batch's colptr loads
@@ -287,12 +335,9 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
-              if (ps[u].j != 0xffffffffu) {
-                const T cval = contrib<CK, T>(x, ps[u].v, p);
-                const uint32_t ad = acc_s + ps[u].j * ES;
-                sts(ad, add_rn(lds(ad, T(0)), cval));
-                if constexpr (KL) sts(cnt_s + ps[u].j * ES, add_rn(lds(cnt_s + ps[u].j * ES, T(0)), T(1)));
-              }
+              uint32_t xr = 0;
+              if constexpr (MX) xr = __shfl_sync(FULL, cur_ar, (q0 + u) & 31);
+              if (ps[u].j != 0xffffffffu) apply_posting(ps[u].j, ps[u].v, x, xr);
               __syncwarp();
             }
           } else {
@@ -300,20 +345,16 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
             for (int u = 0; u < U; ++u) {
               if (q0 + u < ncol) {
                 const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
-                if (ps[u].j != 0xffffffffu) {
-                  const T cval = contrib<CK, T>(x, ps[u].v, p);
-                  const uint32_t ad = acc_s + ps[u].j * ES;
-                  sts(ad, add_rn(lds(ad, T(0)), cval));
-                  if constexpr (KL) sts(cnt_s + ps[u].j * ES, add_rn(lds(cnt_s + ps[u].j * ES, T(0)), T(1)));
-                }
+                uint32_t xr = 0;
+                if constexpr (MX) xr = __shfl_sync(FULL, cur_ar, (q0 + u) & 31);
+                if (ps[u].j != 0xffffffffu) apply_posting(ps[u].j, ps[u].v, x, xr);
                 if (long_mask & (1u << ((q0 + u) & 31))) {  // > 32 postings of this column in this tile
                   const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
                   const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
                   for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
-                    const Posting<T> q2 = load_posting(post + p2);
-                    const uint32_t ad = acc_s + q2.j * ES;
-                    sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, q2.v, p)));
-                    if constexpr (KL) sts(cnt_s + q2.j * ES, add_rn(lds(cnt_s + q2.j * ES, T(0)), T(1)));
+                    Posting<T> q2 = load_posting(post + p2);
+                    if constexpr (MX) q2.j |= uint32_t(a.post_rank[p2]) << 16;
+                    apply_posting(q2.j, q2.v, x, xr);
                   }
                 }
                 __syncwarp();
@@ -359,7 +400,41 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
         const int q = qb + 4 * lane;
         const bool full = q + 3 < nt;
         T r[4];
-        if constexpr (M == SD_M_COSINE) {
+        if constexpr (MX) {  // max(M_isect, largest |a| not hit, largest |b| not hit)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t mk = to_mask(gcv[u]);
+            const int fa = __ffs(~(mk & 0xffffu)) - 1;            // first unhit A rank, 16 = all hit
+            const int fb = __ffs(~(mk >> 16)) - 1;
+            const T ma = __shfl_sync(FULL, topa_l, fa & 31);
+            const int64_t j = j0 + q + u;
+            T mb = gb0[u];                                         // rank 0 of B row j
+            bool exact = fa == CHEB_K && aend - abeg > CHEB_K;
+            if (q + u < nt && fb > 0) {
+              if (fb < CHEB_K) mb = a.topb[int64_t(fb) * a.n + j];
+              else if (a.b_ptr[j + 1] - a.b_ptr[j] > CHEB_K) exact = true;
+              else mb = T(0);
+            }
+            if (exact && q + u < nt) {  // every top-K entry intersects: exact sorted merge (rare)
+              T mx = T(0);
+              int64_t ia = abeg, ib = a.b_ptr[j];
+              const int64_t ie = aend, be = a.b_ptr[j + 1];
+              while (ia < ie || ib < be) {
+                const int32_t ca = ia < ie ? a.a_idx[ia] : INT32_MAX;
+                const int32_t cb = ib < be ? a.b_idx[ib] : INT32_MAX;
+                T dv;
+                if (ca == cb) { dv = abs_(sub_rn(a.a_val[ia], a.b_val[ib])); ++ia; ++ib; }
+                else if (ca < cb) { dv = abs_(a.a_val[ia]); ++ia; }
+                else { dv = abs_(a.b_val[ib]); ++ib; }
+                mx = dv > mx ? dv : mx;
+              }
+              r[u] = mx;
+            } else {
+              T x = gv[u] > ma ? gv[u] : ma;
+              r[u] = mb > x ? mb : x;
+            }
+          }
+        } else if constexpr (M == SD_M_COSINE) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (ra0 > T(0)) {
@@ -444,7 +519,8 @@ __global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __re
 
 template <typename T, int M, int KPL>
 int launch_isect_kernel(IsectArgs<T>& args, int W, cudaStream_t st) {
-  const int64_t per_warp = int64_t(args.tile) * sizeof(T) * (metric_contrib(M) == C_KL ? 2 : 1);
+  const int64_t per_warp = int64_t(args.tile) * sizeof(T) *
+                           ((metric_contrib(M) == C_KL || metric_contrib(M) == C_MAX) ? 2 : 1);
   const size_t smem = size_t(W) * per_warp;
   SD_TRY(prepare_smem(isect_kernel<T, M, KPL>, smem, "isect_kernel"));
   int per_sm = 0;
@@ -476,6 +552,7 @@ int launch_isect_metric(IsectArgs<T>& args, int W, cudaStream_t st) {
       case SD_M_KL: return launch_isect_metric<T, SD_M_KL>(args, W, st);                           \
       case SD_M_RUSSELRAO: return launch_isect_metric<T, SD_M_RUSSELRAO>(args, W, st);             \
       case SD_M_CANBERRA: return launch_isect_metric<T, SD_M_CANBERRA>(args, W, st);               \
+      case SD_M_CHEBYSHEV: return launch_isect_metric<T, SD_M_CHEBYSHEV>(args, W, st);             \
       case SD_M_HAMMING: return launch_isect_metric<T, SD_M_HAMMING>(args, W, st);                 \
       case SD_M_JENSENSHANNON: return launch_isect_metric<T, SD_M_JENSENSHANNON>(args, W, st);     \
       case SD_M_MANHATTAN: return launch_isect_metric<T, SD_M_MANHATTAN>(args, W, st);             \

@@ -98,7 +98,8 @@ __device__ __forceinline__ T expand_cell(int metric, T d, T a0, T a1, T b0, T b1
 }
 
 // ---- contributions of one intersecting column for the fused path
-enum ContribKind { C_MUL = 0, C_KL = 1, C_ABS = 2, C_ABSPOW = 3, C_CANBERRA = 4, C_MISMATCH = 5, C_JS = 6 };
+enum ContribKind { C_MUL = 0, C_KL = 1, C_ABS = 2, C_ABSPOW = 3, C_CANBERRA = 4, C_MISMATCH = 5, C_JS = 6,
+                   C_MAX = 7 /* chebyshev: running max over intersections + top-K hit masks */ };
 
 __host__ __device__ constexpr int metric_contrib(int metric) {
   switch (metric) {
@@ -108,7 +109,7 @@ __host__ __device__ constexpr int metric_contrib(int metric) {
     case SD_M_CANBERRA: return C_CANBERRA;
     case SD_M_HAMMING: return C_MISMATCH;
     case SD_M_JENSENSHANNON: return C_JS;
-    case SD_M_CHEBYSHEV: return -1;  // max-reduce: not decomposable, engine path
+    case SD_M_CHEBYSHEV: return C_MAX;
     default: return C_MUL;
   }
 }
@@ -131,6 +132,8 @@ __device__ __forceinline__ T contrib(T a, T b, T p) {
     return mul_rn(a, b);
   } else if constexpr (CK == C_KL) {
     return product<SD_SR_KL_TERM, T>(a, b, p);
+  } else if constexpr (CK == C_MAX) {
+    return abs_(sub_rn(a, b));
   } else {
     constexpr int SR = CK == C_ABS ? SD_SR_ABS_DIFF
                      : CK == C_ABSPOW ? SD_SR_ABS_DIFF_POW

@@ -15,7 +15,7 @@ template <typename T, int KIND, int SR>
 __device__ __forceinline__ T stat_term(T v, T p) {
   if constexpr (KIND == SD_STAT_L0) return T(1);
   else if constexpr (KIND == SD_STAT_L1) return abs_(v);
-  else if constexpr (KIND == SD_STAT_L2 || KIND == SD_STAT_L2SQ || KIND == STAT_INV_L2) return mul_rn(v, v);
+  else if constexpr (KIND == SD_STAT_L2 || KIND == SD_STAT_L2SQ) return mul_rn(v, v);
   else if constexpr (KIND == SD_STAT_SUM) return v;
   else if constexpr (KIND == STAT_ONESIDED_A) return product<SR, T>(v, T(0), p);
   else return product<SR, T>(T(0), v, p);  // STAT_ONESIDED_B
@@ -35,7 +35,7 @@ constexpr int STAT_WARPS = 4;
 template <typename T, int KIND, int SR>
 __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t* __restrict__ ptr,
                                                                    const T* __restrict__ val, int64_t n_rows,
-                                                                   T p, T* __restrict__ out) {
+                                                                   T p, T* __restrict__ out, T* __restrict__ out2) {
   __shared__ T stage[STAT_WARPS][STAT_CHUNK];
   const unsigned lane = lane_id();
   const int w = threadIdx.x >> 5;
@@ -90,24 +90,28 @@ __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t
         if (int(lane) == src) s = ls;
       }
       if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
-      if constexpr (KIND == STAT_INV_L2) {
-        s = sqrt_rn(s);
-        s = s > T(0) ? div_rn(T(1), s) : T(0);
-      }
     }
-    if (ok) out[r] = s;
+    if (ok) {
+      out[r] = s;
+      if constexpr (KIND == SD_STAT_L2)  // optional 1/||row|| (0 for empty rows), same pass
+        if (out2) out2[r] = s > T(0) ? div_rn(T(1), s) : T(0);
+    }
   }
 }
 
 template <typename T, int KIND, int SR>
-static int launch_stat(const sd_csr* m, T p, void* out, cudaStream_t st) {
+static int launch_stat(const sd_csr* m, T p, void* out, cudaStream_t st, void* out2 = nullptr) {
   if (m->n_rows == 0) return SD_OK;
   const int64_t warps = (m->n_rows + 31) / 32;
   int blocks = int(tmin<int64_t>((warps + STAT_WARPS - 1) / STAT_WARPS, int64_t(num_sms()) * 16));
   row_stat_kernel<T, KIND, SR><<<blocks, STAT_WARPS * 32, 0, st>>>(
-      m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out));
+      m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out), static_cast<T*>(out2));
   SD_LAUNCH_CHECK();
   return SD_OK;
+}
+
+int row_stat_l2_inv(const sd_csr* m, int dtype, void* l2, void* inv, cudaStream_t st) {
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int { return launch_stat<T, SD_STAT_L2, 0>(m, T(0), l2, st, inv); });
 }
 
 int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void* out,
@@ -120,7 +124,6 @@ int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void*
       case SD_STAT_L2: return launch_stat<T, SD_STAT_L2, 0>(m, pp, out, st);
       case SD_STAT_L2SQ: return launch_stat<T, SD_STAT_L2SQ, 0>(m, pp, out, st);
       case SD_STAT_SUM: return launch_stat<T, SD_STAT_SUM, 0>(m, pp, out, st);
-      case STAT_INV_L2: return launch_stat<T, STAT_INV_L2, 0>(m, pp, out, st);
       case STAT_ONESIDED_A:
         return SD_DISPATCH_SEMIRING(semiring, SR, [&]() -> int { return launch_stat<T, STAT_ONESIDED_A, SR>(m, pp, out, st); });
       case STAT_ONESIDED_B:
@@ -129,6 +132,60 @@ int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void*
         set_error("unknown row statistic kind");
         return SD_E_INVALID;
     }
+  });
+}
+
+// Per-row top-K by |value| (ties -> lower entry index): rank[e] in [0, K) for
+// the K largest entries of each row, 255 otherwise; top[r * n_rows + row] =
+// the r-th largest |value| (0 beyond the row's degree).  Used by the fused
+// Chebyshev path (max over the union needs the largest one-sided entries).
+template <typename T>
+__global__ void row_topk_kernel(const int64_t* __restrict__ ptr, const T* __restrict__ val, int64_t n_rows,
+                                uint8_t* __restrict__ rank, T* __restrict__ top) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  for (int64_t row = warp; row < n_rows; row += nw) {
+    const int64_t beg = ptr[row], end = ptr[row + 1];
+    for (int64_t e = beg + lane; e < end; e += 32) rank[e] = 255;
+    __syncwarp();
+    T prev_k = Num<T>::inf();
+    int64_t prev_e = -1;
+    for (int r = 0; r < CHEB_K; ++r) {
+      // next entry in (|v| desc, e asc) order after (prev_k, prev_e)
+      T best_k = T(-1);
+      int64_t best_e = INT64_MAX;
+      for (int64_t e = beg + lane; e < end; e += 32) {
+        const T k = abs_(val[e]);
+        const bool after = k < prev_k || (k == prev_k && e > prev_e);
+        if (after && (k > best_k || (k == best_k && e < best_e))) { best_k = k; best_e = e; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const T ok = __shfl_xor_sync(0xffffffffu, best_k, o);
+        const int64_t oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+        if (ok > best_k || (ok == best_k && oe < best_e)) { best_k = ok; best_e = oe; }
+      }
+      if (lane == 0) top[int64_t(r) * n_rows + row] = best_e == INT64_MAX ? T(0) : best_k;
+      if (best_e == INT64_MAX) {  // row exhausted
+        for (int rr = r + 1 + int(lane); rr < CHEB_K; rr += 32) top[int64_t(rr) * n_rows + row] = T(0);
+        break;
+      }
+      if (lane == 0) rank[best_e] = uint8_t(r);
+      prev_k = best_k;
+      prev_e = best_e;
+    }
+  }
+}
+
+int row_topk(const sd_csr* m, int dtype, uint8_t* rank, void* top, cudaStream_t st) {
+  if (m->n_rows == 0) return SD_OK;
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    const int blocks = int(tmin<int64_t>((m->n_rows * 32 + 255) / 256, int64_t(num_sms()) * 16));
+    row_topk_kernel<T><<<blocks, 256, 0, st>>>(m->indptr, static_cast<const T*>(m->values), m->n_rows, rank,
+                                               static_cast<T*>(top));
+    SD_LAUNCH_CHECK();
+    return SD_OK;
   });
 }
 

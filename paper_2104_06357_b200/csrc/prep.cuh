@@ -15,12 +15,17 @@ struct Stats {  // per-row statistics the metric epilogue reads (metric.cuh layo
 //   S_A[i] = sum_c ⊗(a_ic, 0)   and   S_B[j] = sum_c ⊗(0, b_jc)
 constexpr int STAT_ONESIDED_A = 16;
 constexpr int STAT_ONESIDED_B = 17;
-// 1/||row||_2 (0 for an empty row): the fused cosine epilogue multiplies instead of dividing
-constexpr int STAT_INV_L2 = 18;
+
 
 int row_stat(const sd_csr* m, int dtype, int kind, int semiring, double p, void* out,
              cudaStream_t st);
 int csr_to_coo(const sd_csr* m, int64_t* rows, cudaStream_t st);
+// ||row||_2 and 1/||row||_2 (0 for empty rows) in one pass: the fused cosine
+// epilogue multiplies by reciprocals instead of dividing
+int row_stat_l2_inv(const sd_csr* m, int dtype, void* l2, void* inv, cudaStream_t st);
+// fused Chebyshev: per-row top-CHEB_K entries by |value|
+constexpr int CHEB_K = 16;
+int row_topk(const sd_csr* m, int dtype, uint8_t* rank, void* top, cudaStream_t st);
 int check_nonnegative(const sd_csr* m, int dtype, uint32_t* flags, cudaStream_t st);
 int sqrt_values(const sd_csr* m, int dtype, void* out, cudaStream_t st);
 int fill(void* out, int64_t m, int64_t n, int64_t ldo, int dtype, double value, cudaStream_t st);

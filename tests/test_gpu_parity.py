@@ -318,3 +318,27 @@ def test_sharded_knn_emulated_on_one_gpu():
         base = sd.kneighbors(x, q, k, spec)
         np.testing.assert_array_equal(mi.cpu().numpy(), base.indices)
         np.testing.assert_array_equal(md.cpu().numpy(), base.distances)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_fused_chebyshev_matches_engine_and_oracle(dtype):
+    """Fused chebyshev (max over intersections + top-16 hit masks, exact merge
+    when a row's top-16 all intersect) against the oracle, incl. rows dense
+    enough to force the exact fallback."""
+    rng = np.random.default_rng(41)
+    for dens in (0.05, 0.3, 0.9):
+        da = np.where(rng.random((40, 64)) < dens, rng.uniform(-1, 1, (40, 64)), 0.0)
+        db = np.where(rng.random((70, 64)) < dens, rng.uniform(-1, 1, (70, 64)), 0.0)
+        db[:5] = da[:5]                      # identical rows: every entry intersects
+        a, b = _f32(sd.from_dense(da)), _f32(sd.from_dense(db))
+        ref = O.pairwise_distances(a, b, "chebyshev")
+        got = sd.pairwise_distances(a, b, sd.metric_registry("chebyshev"), dtype=dtype)
+        if dtype == np.float64:
+            np.testing.assert_array_equal(got, ref)
+        else:
+            np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-7)
+        eng = sd.pairwise_distances(a, b, sd.metric_registry("chebyshev"), "dense", dtype=dtype)
+        np.testing.assert_array_equal(got, eng)
+        res = sd.kneighbors(b, a, 5, sd.metric_registry("chebyshev"), dtype=dtype)
+        ref_d, ref_i = O.kneighbors(b, a, 5, "chebyshev")
+        assert_knn_parity(res.distances, res.indices, ref_d, ref_i, ref, tol=1e-6)
