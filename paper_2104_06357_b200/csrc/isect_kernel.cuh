@@ -75,8 +75,8 @@ template <> struct V4<float> {
     const float4 t = *reinterpret_cast<const float4*>(p);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   }
-  __device__ __forceinline__ static void store(float* p, const float* v) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  __device__ __forceinline__ static void store(float* p, const float* v) {  // streaming store
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
   }
 };
 template <> struct V4<double> {
@@ -86,15 +86,17 @@ template <> struct V4<double> {
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   }
   __device__ __forceinline__ static void store(double* p, const double* v) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    __stcs(reinterpret_cast<double2*>(p) + 1, make_double2(v[2], v[3]));
   }
 };
 
 // read-only 8/16-byte posting fetch (ld.global.nc)
+// postings are re-read by every query touching a column: keep them in L2
+// (evict_last) against the output stream, which is written evict_first
 __device__ __forceinline__ Posting<float> load_posting(const Posting<float>* p) {
   uint2 r;
-  asm("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  asm("ld.global.nc.L2::evict_last.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   Posting<float> q;
   q.j = r.x;
   q.v = __uint_as_float(r.y);
@@ -102,7 +104,7 @@ __device__ __forceinline__ Posting<float> load_posting(const Posting<float>* p) 
 }
 __device__ __forceinline__ Posting<double> load_posting(const Posting<double>* p) {
   unsigned long long a, b;
-  asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  asm("ld.global.nc.L2::evict_last.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
   Posting<double> q;
   q.j = uint32_t(a);
   q.pad = 0;
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
           } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (q + u < nt) orow[q + u] = r[u];
+              if (q + u < nt) __stcs(orow + q + u, r[u]);
           }
         }
       };
