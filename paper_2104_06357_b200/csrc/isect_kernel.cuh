@@ -94,17 +94,22 @@ template <> struct V4<double> {
 // read-only 8/16-byte posting fetch (ld.global.nc)
 // postings are re-read by every query touching a column: keep them in L2
 // (evict_last) against the output stream, which is written evict_first
-__device__ __forceinline__ Posting<float> load_posting(const Posting<float>* p) {
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ Posting<float> load_posting(const Posting<float>* p, uint64_t pol) {
   uint2 r;
-  asm("ld.global.nc.L2::evict_last.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
   Posting<float> q;
   q.j = r.x;
   q.v = __uint_as_float(r.y);
   return q;
 }
-__device__ __forceinline__ Posting<double> load_posting(const Posting<double>* p) {
+__device__ __forceinline__ Posting<double> load_posting(const Posting<double>* p, uint64_t pol) {
   unsigned long long a, b;
-  asm("ld.global.nc.L2::evict_last.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  asm("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(a), "=l"(b) : "l"(p), "l"(pol));
   Posting<double> q;
   q.j = uint32_t(a);
   q.pad = 0;
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
                : "r"(uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(warp) * TJ * ES * (KL ? 2u : 1u)));
   const uint32_t cnt_s = acc_s + uint32_t(TJ) * ES;
   const Posting<T>* __restrict__ post = a.post;
+  const uint64_t l2pol = l2_evict_last_policy();
   const T p = a.p;
   const int64_t band_items = a.item_off[a.m];  // written by plan_kernel
   const int64_t total_items = a.tile_major ? band_items : band_items * ((a.n_tiles + a.band - 1) / a.band);
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               const uint32_t pp = b0 + lane;
               ps[u].j = 0xffffffffu;
               if (pp < b1) {
-                ps[u] = load_posting(post + pp);
+                ps[u] = load_posting(post + pp, l2pol);
                 if constexpr (MX) ps[u].j |= uint32_t(a.post_rank[pp]) << 16;
               }
             }
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               const uint32_t pp = b0 + lane;
               ps[u].j = 0xffffffffu;
               if (q0 + u < ncol && pp < b1) {
-                ps[u] = load_posting(post + pp);
+                ps[u] = load_posting(post + pp, l2pol);
                 if constexpr (MX) ps[u].j |= uint32_t(a.post_rank[pp]) << 16;
               }
             }
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
                   const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
                   const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
                   for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
-                    Posting<T> q2 = load_posting(post + p2);
+                    Posting<T> q2 = load_posting(post + p2, l2pol);
                     if constexpr (MX) q2.j |= uint32_t(a.post_rank[p2]) << 16;
                     apply_posting(q2.j, q2.v, x, xr);
                   }
