@@ -283,8 +283,12 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   const int W = int(std::min<int64_t>(ISECT_MAX_WARPS, (smem_optin_bytes() - 2048) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const int64_t warps = int64_t(num_sms()) * W;
+  // band of tiles whose postings (~100 MB) stay L2-resident while all queries
+  // sweep it; SD_ISECT_BAND overrides (tuning)
   const char* be0 = getenv("SD_ISECT_BAND");
-  const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : ix->n_tiles));
+  const int64_t post_bytes = std::max<int64_t>(1, ix->bytes);
+  const int64_t auto_band = (ix->n_tiles * int64_t(100) * 1000 * 1000 + post_bytes - 1) / post_bytes;
+  const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : auto_band));
   const int64_t max_items = m * band0 * ((ix->n_tiles + band0 - 1) / band0);
   Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
   SD_TRY(order.alloc(sizeof(int32_t) * m, st));
@@ -295,8 +299,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   SD_CUDA_TRY(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int), st));
   const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
   const int tile_major = pe ? atoi(pe) : 0;
-  const char* be = getenv("SD_ISECT_BAND");  // tiles per band (L2-resident posting working set)
-  const int64_t band = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be ? atoll(be) : ix->n_tiles));
+  const int64_t band = band0;
   plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
                                   order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
                                   item_pos.as<int32_t>());
