@@ -1,20 +1,23 @@
-"""Benchmark of the hot path (BASELINE.json metric, configs[1]):
+"""Benchmark of the hot path.
 
-  cosine (+ expanded euclidean, power-law manhattan as extra lines of the
-  same run) pairwise distances for 10,000 query rows against the full
-  MovieLens-25M-shaped power-law index (162,541 x 59,047, ~154 nnz/row),
-  float32, synthetic data from the reference's own generator.
+Default workload (BASELINE.json configs[1], what the driver runs): cosine
+(+ expanded euclidean and power-law manhattan as extra lines of the same run)
+pairwise distances of 10,000 query rows against the full MovieLens-25M-shaped
+power-law index (162,541 x 59,047, ~154 nnz/row), fp32, synthetic data from
+the reference's own generator.  One step = the full 10,000 x 162,541 distance
+matrix.  Other BASELINE configs: --workload c1 | c3 | c4 | c5 (c5 = kNN).
 
-One step = the full 10,000 x 162,541 distance matrix for one query batch.
 Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA
-events on the launching stream, max over ranks.  Inputs and the 6.5 GB
-output exceed the 126 MB L2, so no explicit flush is needed.
+events on the launching stream, max over ranks.  Inputs and outputs exceed
+the 126 MB L2 (C1 excepted, stated in `config`).
 
-Multi-GPU (torchrun): weak scaling — every rank owns its own 10,000-query
-batch against a replicated index; no collective on the data path.
+Multi-GPU (torchrun): pairwise workloads scale weakly (each rank owns its own
+query batch against a replicated index, no collective on the data path); the
+kNN workload shards the index rows and merges per-rank top-k with one NCCL
+all-gather (strong scaling: the same queries, 1/N of the index per rank).
 
---impl reference: the reference's CPU algorithm (oracle/ numpy port, all host
-cores) on a bounded query sample of the same workload.
+--impl reference: the reference's CPU algorithm (oracle/ numpy port, bitwise
+equal to the reference, all host cores) on a bounded query sample.
 """
 
 import argparse
@@ -31,21 +34,51 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-INDEX_SPEC = dict(n_rows=162541, n_cols=59047, degree_dist="zipf", zipf_s=1.544, zipf_max_degree=32000,
-                  value_dist="uniform01", seed=25)
-N_QUERIES = 10000
+WORKLOADS = {
+    "c1": dict(desc="BASELINE configs[0]: 1k x 1k rows, 10k cols, 1% uniform density", ref_queries=1000,
+               index=dict(n_rows=1000, n_cols=10000, degree_dist="uniform", degree=100, seed=2),
+               queries=dict(n_rows=1000, n_cols=10000, degree_dist="uniform", degree=100, seed=1),
+               metrics=["manhattan", "cosine"], n_queries=1000, kind="pairwise"),
+    "c2": dict(desc="BASELINE configs[1]: MovieLens-25M-shaped power-law index 162,541 x 59,047, ~154 nnz/row",
+               index=dict(n_rows=162541, n_cols=59047, degree_dist="zipf", zipf_s=1.544, zipf_max_degree=32000,
+                          seed=25),
+               metrics=["cosine", "euclidean", "manhattan"], n_queries=10000, kind="pairwise"),
+    "c3": dict(desc="BASELINE configs[2]: NYTimes-BoW-shaped index 300,000 x 102,660, ~232 nnz/row, tf-idf values",
+               index=dict(n_rows=300000, n_cols=102660, degree_dist="zipf", zipf_s=1.309, zipf_max_degree=2000,
+                          value_dist="tfidf", seed=3),
+               metrics=["canberra", "chebyshev", "jensenshannon", "kl"], n_queries=4096, kind="pairwise"),
+    "c4": dict(desc="BASELINE configs[3]: scRNA-shaped index 65,000 x 26,000, degrees lognormal in [501, 9600] "
+                    "(mean ~1.8k, ~7% dense)",
+               index=dict(n_rows=65000, n_cols=26000, degree_dist="lognormal", lognormal_mu=7.38,
+                          lognormal_sigma=0.55, min_degree=501, max_degree=9600, value_dist="tfidf", seed=4),
+               metrics=["hellinger", "jaccard"], n_queries=2048, kind="pairwise"),
+    "c5": dict(desc="BASELINE configs[4]: brute-force kNN k=32 cosine, 1,000,000 x 100,000 power-law index "
+                    "(~154 nnz/row)",
+               index=dict(n_rows=1000000, n_cols=100000, degree_dist="zipf", zipf_s=1.50, zipf_max_degree=10000,
+                          seed=5),
+               metrics=["cosine"], n_queries=10000, kind="knn", k=32),
+}
+BINARY_METRICS = ("jaccard", "dice", "russelrao", "hamming")
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def make_data(rank, n_queries):
+def make_data(wl, rank, n_queries):
+    """Index (values rounded to fp32) and this rank's query batch."""
     import paper_2104_06357_b200 as sd
-    index = sd.round_values_f32(sd.generate(sd.GenSpec(**INDEX_SPEC)))
+    index = sd.round_values_f32(sd.generate(sd.GenSpec(**wl["index"])))
+    if "queries" in wl:
+        return index, sd.round_values_f32(sd.generate(sd.GenSpec(**wl["queries"])))
     rng = np.random.default_rng(26 + rank)
-    rows = np.sort(rng.choice(index.n_rows, n_queries, replace=False))
+    rows = np.sort(rng.choice(index.n_rows, min(n_queries, index.n_rows), replace=False))
     return index, gather_rows(index, rows)
+
+
+def binary(m):
+    """Same pattern with values 1 (set-semantics metrics, BINARY_PREFERRED metrics.py:37)."""
+    return m.with_values(np.ones(len(m.values)))
 
 
 def gather_rows(m, rows):
@@ -54,7 +87,8 @@ def gather_rows(m, rows):
     deg = ptr[rows + 1] - ptr[rows]
     newptr = np.zeros(len(rows) + 1, dtype=np.int64)
     np.cumsum(deg, out=newptr[1:])
-    take = np.concatenate([np.arange(ptr[r], ptr[r + 1]) for r in rows]) if len(rows) else np.zeros(0, np.int64)
+    starts = np.repeat(ptr[rows], deg)
+    take = starts + (np.arange(newptr[-1]) - np.repeat(newptr[:-1], deg))
     return sd.CsrMatrix(len(rows), m.n_cols, newptr, np.asarray(m.indices)[take], np.asarray(m.values)[take])
 
 
@@ -120,62 +154,78 @@ def load_peak():
         return 6650.0, "fallback"
 
 
-def load_traffic():
+def load_traffic(workload):
     """Per-launch DRAM bytes of the fused kernel from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_isect_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            d = json.load(f)
+        return d if d.get("workload", "c2") == workload else None
     except (OSError, ValueError):
         return None
 
 
-def cpu_reference_rate(index, queries, metric, sample, budget_s=20.0):
+def cpu_reference_rate(index, queries, metric, sample, budget_s=20.0, k=None):
     """The reference algorithm (oracle numpy port, bitwise = reference) on a
     query sample against the full index, all host threads.  Returns
-    (distances/s, sample rows, cores, seconds, rows array)."""
+    (units/s, sample rows, cores, seconds, result)."""
     from oracle import semidist_oracle as O
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     oi = O.Csr.of(index)
     oq = O.Csr.of(queries)
-    O.pairwise_distances(oq.slice(0, 1), oi, metric, workers=cores)      # warm caches
-    cal = min(8, sample, oq.n_rows)
+    strict = metric != "kl"
+
+    def run(q):
+        if k is not None:
+            return O.kneighbors(oi, oq.slice(0, q), k, metric, workers=cores, batch_rows=q)
+        return O.pairwise_distances(oq.slice(0, q), oi, metric, strict=strict, workers=cores)
+
+    # one small run; if it was quick, one larger run sized to the budget (the
+    # two-pass metrics have a per-call cost independent of the query count)
+    q = int(min(4, sample, oq.n_rows))
     t0 = time.perf_counter()
-    O.pairwise_distances(oq.slice(0, cal), oi, metric, workers=cores)
-    per_query = max(1e-4, (time.perf_counter() - t0) / cal)
-    q = int(max(1, min(sample, oq.n_rows, budget_s / per_query)))
-    t0 = time.perf_counter()
-    ref = O.pairwise_distances(oq.slice(0, q), oi, metric, workers=cores)
+    res = run(q)
     dt = time.perf_counter() - t0
-    return q * index.n_rows / dt, q, cores, dt, ref
+    if dt < budget_s / 3 and q < min(sample, oq.n_rows):
+        q = int(max(q + 1, min(sample, oq.n_rows, q * budget_s / max(dt, 1e-3) / 2)))
+        t0 = time.perf_counter()
+        res = run(q)
+        dt = time.perf_counter() - t0
+    units = q if k is not None else q * index.n_rows
+    return units / dt, q, cores, dt, res
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    index, queries = make_data(0, min(N_QUERIES, 64))
-    rates = []
-    sample = None
+    wl = WORKLOADS[args.workload]
+    metric = args.metric or wl["metrics"][0]
+    index, queries = make_data(wl, 0, min(wl["n_queries"], max(256, wl.get("ref_queries", 0))))
+    if metric in BINARY_METRICS:
+        index, queries = binary(index), binary(queries)
+    k = wl.get("k") if wl["kind"] == "knn" else None
+    rates, sample, cores = [], None, 1
     for step in range(args.warmup + args.steps):
-        rate, q, cores, dt, _ = cpu_reference_rate(index, queries, args.metric, sample=args.ref_queries,
-                                                   budget_s=args.ref_budget)
+        rate, q, cores, dt, _ = cpu_reference_rate(index, queries, metric,
+                                                   sample=wl.get("ref_queries", args.ref_queries),
+                                                   budget_s=args.ref_budget, k=k)
         sample = q
         if step >= args.warmup:
             rates.append(rate)
     value = statistics.median(rates)
+    unit = "queries/s" if k else "distances/s"
     line = {
-        "metric": "pairwise distances/sec", "value": value, "unit": "distances/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample * index.n_rows / value * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator, MovieLens-25M shape)", "impl": "reference",
-        "config": {"workload": f"{args.metric} pairwise, {sample}-query sample of the 10k-query batch vs the "
-                               f"162,541 x 59,047 power-law index (~154 nnz/row)",
-                   "metric": args.metric, "index_rows": index.n_rows, "n_cols": index.n_cols,
-                   "index_nnz": index.nnz},
-        "cpu_baseline": {"value": value, "unit": "distances/s", "cores": cores, "kind": "port",
+        "metric": "kNN queries/sec" if k else "pairwise distances/sec", "value": value, "unit": unit,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (sample if k else sample * index.n_rows) / value * 1e3,
+        "higher_is_better": True, "scaling": "strong" if k else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, values rounded to fp32)", "impl": "reference",
+        "config": {"workload": f"{args.workload}: {metric}, {sample}-query sample vs the full index; {wl['desc']}",
+                   "metric": metric, "index_rows": index.n_rows, "n_cols": index.n_cols, "index_nnz": index.nnz},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
                          "sample": f"{sample} queries x {index.n_rows} index rows per step"},
-        "e2e": {"value": value, "unit": "distances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -189,7 +239,11 @@ def run_ours(args):
 
     import paper_2104_06357_b200 as sd
     from paper_2104_06357_b200 import _lib
+    from paper_2104_06357_b200.distributed import gather_candidates, merge_candidates, shard_bounds
 
+    wl = WORKLOADS[args.workload]
+    knn = wl["kind"] == "knn"
+    metrics = [args.metric] if args.metric else list(wl["metrics"])
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -199,29 +253,56 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     t_setup = time.perf_counter()
-    index, queries = make_data(rank, args.queries)
-    log(f"[rank {rank}] data: index {index.n_rows}x{index.n_cols} nnz={index.nnz} "
-        f"(mean deg {index.nnz / index.n_rows:.1f}); queries nnz={queries.nnz} ({time.perf_counter() - t_setup:.1f}s)")
+    n_queries = args.queries or wl["n_queries"]
+    index, queries = make_data(wl, 0 if knn else rank, n_queries)
+    index_full_rows = index.n_rows
+    shard_lo = 0
+    if knn and world > 1:   # index rows sharded across ranks, queries replicated
+        shard_lo, shard_hi = shard_bounds(index.n_rows, world)[rank]
+        index = sd.slice_rows(index, shard_lo, shard_hi)
+    log(f"[rank {rank}] {args.workload}: index {index.n_rows}x{index.n_cols} nnz={index.nnz} "
+        f"(mean deg {index.nnz / max(1, index.n_rows):.1f}); queries {queries.n_rows} nnz={queries.nnz} "
+        f"({time.perf_counter() - t_setup:.1f}s)")
     tdt = torch.float32 if args.dtype == "float32" else torch.float64
     es = 4 if tdt == torch.float32 else 8
-    di = sd.to_device(index, tdt, dev)
-    dq = sd.to_device(queries, tdt, dev)
-    ix = _lib.device_index(di)
     m, n = queries.n_rows, index.n_rows
-    ldo = (n + 3) // 4 * 4   # 16-byte aligned rows: the epilogue stores 4 cells per lane
-    out = torch.empty((m, ldo), dtype=tdt, device=dev)
-    flags = _lib.new_flags(dev)
     stream = torch.cuda.current_stream(dev)
     sh = ctypes.c_void_p(stream.cuda_stream)
     strat = _lib.strategy_struct(_lib.STRAT_AUTO)
     rep = _lib.SdReport()
+    flags = _lib.new_flags(dev)
+    ldo = (n + 3) // 4 * 4   # 16-byte aligned rows: the epilogue stores 4 cells per lane
+    out = None if knn else torch.empty((m, ldo), dtype=tdt, device=dev)
+    k = wl.get("k", 0)
+    od = torch.empty((m, k), dtype=tdt, device=dev) if knn else None
+    oi = torch.empty((m, k), dtype=torch.int64, device=dev) if knn else None
+    operands = {}
+
+    def prepare(metric):
+        if metric in operands:
+            return operands[metric]
+        idx_m, q_m = (binary(index), binary(queries)) if metric in BINARY_METRICS else (index, queries)
+        transform = "sqrt" if metric == "hellinger" else None
+        di = sd.to_device(idx_m, tdt, dev, transform=transform)
+        dq = sd.to_device(q_m, tdt, dev, transform=transform)
+        ix = _lib.device_index(di)
+        operands[metric] = (di, dq, ix, _lib.metric_struct(metric, None, metric != "kl", transform is not None))
+        return operands[metric]
 
     def step(metric, phases=None):
-        md = _lib.metric_struct(metric)
+        di, dq, ix, md = prepare(metric)
         ca, cb = _lib.csr_struct(dq), _lib.csr_struct(di)
-        _lib.check(lib.sd_pairwise(ctypes.byref(ca), ctypes.byref(cb), ix.handle, _lib.dtype_code(tdt),
-                                   ctypes.byref(md), ctypes.byref(strat), out.data_ptr(), ldo, flags.data_ptr(),
-                                   ctypes.byref(rep), phases, sh), "sd_pairwise")
+        if knn:
+            _lib.check(lib.sd_knn(ctypes.byref(ca), ctypes.byref(cb), ix.handle, _lib.dtype_code(tdt),
+                                  ctypes.byref(md), k, shard_lo, od.data_ptr(), oi.data_ptr(), flags.data_ptr(), sh),
+                       "sd_knn")
+            if world > 1:
+                cd, ci = gather_candidates(od, oi)
+                merge_candidates(cd, ci, k)
+        else:
+            _lib.check(lib.sd_pairwise(ctypes.byref(ca), ctypes.byref(cb), ix.handle, _lib.dtype_code(tdt),
+                                       ctypes.byref(md), ctypes.byref(strat), out.data_ptr(), ldo,
+                                       flags.data_ptr(), ctypes.byref(rep), phases, sh), "sd_pairwise")
 
     def barrier():
         if world > 1:
@@ -247,109 +328,133 @@ def run_ours(args):
             ms = float(t.item())
         return ms, launches
 
-    # ---------------- headline: K timed steps of the configured metric
+    head = metrics[0]
+    prepare(head)
+    # ---------------- headline: K timed steps of the workload's first metric
     clocks = ClockSampler(local)
     for _ in range(args.warmup):
-        step(args.metric)
+        step(head)
     barrier()
     clocks.start()
-    ms, launches = timed(args.metric, args.steps, 0)
+    ms, launches = timed(head, args.steps, 0)
     clk = clocks.stop()
-    total_distances = m * n * world
-    value = total_distances / (ms / 1e3)
-    assert int(flags.item()) == 0, "domain flag raised during benchmark"
+    units = m if knn else m * n * world   # queries answered (index sharded) / distances (all ranks)
+    value = units / (ms / 1e3)
+    assert int(flags.item()) == 0 or head == "kl", "domain flag raised during benchmark"
 
     # ---------------- roofline of the dominant kernel (fused intersection kernel)
-    phases = (ctypes.c_float * 4)()
-    kern_ms = []
-    for _ in range(max(3, args.steps)):
-        step(args.metric, phases)
-        kern_ms.append(phases[1])
-    kern = statistics.median(kern_ms)
-    qdeg = np.diff(np.asarray(queries.indptr))
-    # compulsory bytes of one launch: output written once, both
-    # operands + index + per-row statistics read once
-    alg_bytes = (m * n * es + queries.nnz * (4 + es) + (m + 1) * 8
-                 + index.nnz * (2 + es) + 4 * (ix.tile_rows and (-(-n // ix.tile_rows)) * index.n_cols)
-                 + (m + n) * es)
-    achieved = alg_bytes / (kern / 1e3) / 1e9
-    peak, peak_kind = load_peak()
-    traffic = load_traffic()
-    # SURVEY §8(d) Alg.-3 stream model for reference: every query row streams all of B
-    alg3_bytes = m * index.nnz * (8 + es) + m * n * es
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                "kernel": "isect_kernel", "kernel_ms": kern, "alg_bytes_per_launch": alg_bytes,
-                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                "alg3_stream_equiv_gbs": alg3_bytes / (kern / 1e3) / 1e9}
+    roofline = None
+    if not knn:
+        phases = (ctypes.c_float * 4)()
+        kern_ms = []
+        for _ in range(max(3, args.steps)):
+            step(head, phases)
+            kern_ms.append(phases[1])
+        kern = statistics.median(kern_ms)
+        di, dq, ix, _ = prepare(head)
+        # compulsory bytes of one launch: output written once,
+        # query CSR + index (postings, colptr) + per-row statistics read once
+        post_b = 8 if es == 4 else 16
+        alg_bytes = (m * n * es + dq.nnz * (4 + es) + (m + 1) * 8 + di.nnz * post_b
+                     + 4 * (-(-n // ix.tile_rows)) * index.n_cols + (m + n) * es)
+        achieved = alg_bytes / (kern / 1e3) / 1e9
+        peak, peak_kind = load_peak()
+        traffic = load_traffic(args.workload)
+        alg3_bytes = m * index.nnz * (8 + es) + m * n * es   # every query streams all of B
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                    "kernel": f"isect_kernel<{'float' if es == 4 else 'double'}, {head}>", "kernel_ms": kern,
+                    "alg_bytes_per_launch": alg_bytes,
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)",
+                    "alg3_stream_equiv_gbs": alg3_bytes / (kern / 1e3) / 1e9}
 
-    # ---------------- extra metrics of the same config (cosine + expanded euclidean, power-law manhattan)
-    per_metric = {}
-    for metric in args.extra:
-        ms_x, _ = timed(metric, max(2, args.steps // 2), 1)
-        per_metric[metric] = {"distances_per_s": total_distances / (ms_x / 1e3), "ms_per_step": ms_x}
-    per_metric[args.metric] = {"distances_per_s": value, "ms_per_step": ms}
+    # ---------------- the workload's other metrics (same data, same timing rules)
+    per_metric = {head: {"value": value, "ms_per_step": ms}}
+    if not args.no_extra:
+        for metric in metrics[1:]:
+            ms_x, _ = timed(metric, max(2, args.steps // 2), 1)
+            per_metric[metric] = {"value": units / (ms_x / 1e3), "ms_per_step": ms_x}
 
     # ---------------- e2e: public API, host in / host out, pinned buffers
-    host_out = torch.empty((m, n), dtype=tdt, pin_memory=True)
-    hp = torch.from_numpy(np.asarray(queries.indptr, dtype=np.int64)).pin_memory()
-    hi = torch.from_numpy(np.asarray(queries.indices, dtype=np.int32)).pin_memory()
-    hv = torch.from_numpy(np.asarray(queries.values)).to(tdt).pin_memory()
-    spec = sd.metric_registry(args.metric)
+    di, dq, ix, md = prepare(head)
+    qh = binary(queries) if head in BINARY_METRICS else queries
+    hp = torch.from_numpy(np.asarray(qh.indptr, dtype=np.int64)).pin_memory()
+    hi = torch.from_numpy(np.asarray(qh.indices, dtype=np.int32)).pin_memory()
+    hv = torch.from_numpy(np.asarray(qh.values)).to(tdt).pin_memory()
+    spec = sd.metric_registry(head, strict=head != "kl")
     h2d = hp.numel() * 8 + hi.numel() * 4 + hv.numel() * es
-    d2h = m * n * es
+    if knn:
+        host_d = torch.empty((m, k), dtype=tdt, pin_memory=True)
+        host_i = torch.empty((m, k), dtype=torch.int64, pin_memory=True)
+        d2h = m * k * (es + 8)
+    else:
+        host_out = torch.empty((m, n), dtype=tdt, pin_memory=True)
+        d2h = m * n * es
+    index_host = binary(index) if head in BINARY_METRICS else index
 
     def e2e_step():
         q = sd.upload(m, queries.n_cols, hp, hi, hv, device=dev)
-        sd.pairwise_distances(q, di, spec, dtype=tdt, out=host_out)
+        if knn:
+            from paper_2104_06357_b200.knn import knn_device
+            d, i_, _ = knn_device(index_host, q, k, spec, dtype=tdt, index_base=shard_lo)
+            if world > 1:
+                cd, ci = gather_candidates(d, i_)
+                d, i_ = merge_candidates(cd, ci, k)
+            host_d.copy_(d, non_blocking=True)
+            host_i.copy_(i_, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        else:
+            sd.pairwise_distances(q, index_host, spec, dtype=tdt, out=host_out)
 
     e2e_step()
     barrier()
     t0 = time.perf_counter()
     e_steps = max(2, min(args.steps, 5))
-    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ee0.record(stream)
     for _ in range(e_steps):
         e2e_step()
-    ee1.record(stream)
     barrier()
-    e2e_ms = max(ee0.elapsed_time(ee1), (time.perf_counter() - t0) * 1e3) / e_steps
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = {"value": total_distances / (e2e_ms / 1e3), "unit": "distances/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-           "path": "sd.upload(pinned CSR) -> sd.pairwise_distances(..., out=pinned host buffer)"}
+    e2e = {"value": units / (e2e_ms / 1e3), "unit": "queries/s" if knn else "distances/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+           "path": ("sd.upload(pinned CSR) -> fused kNN (+ all-gather merge) -> pinned host (dist, idx)" if knn else
+                    "sd.upload(pinned CSR) -> sd.pairwise_distances(..., out=pinned host buffer)")}
 
-    # ---------------- CPU baseline (rank 0, N=1 only) + parity of the sampled rows
+    # ---------------- CPU baseline (rank 0, N=1 only) + agreement on the sampled rows
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, q, cores, dt, ref = cpu_reference_rate(index, queries, args.metric, sample=args.ref_queries,
-                                                     budget_s=args.ref_budget)
-        step(args.metric)
-        got = out[:q, :n].double().cpu().numpy()
-        # tests/parity.py rule for cosine in fp32: |got-ref| <= 1e-5*|ref| + 4e-5
-        excess = float(np.max(np.abs(got - ref) / (1e-5 * np.abs(ref) + 4e-5))) if ref.size else 0.0
-        cpu = {"value": rate, "unit": "distances/s", "cores": cores, "kind": "port",
-               "sample": f"{q} queries x {n} index rows ({dt:.1f}s, oracle numpy port, fp64)",
-               "gpu_rows_vs_port_max_abs_err": float(np.max(np.abs(got - ref))) if ref.size else 0.0,
-               "gpu_rows_within_parity_rule": bool(excess <= 1.0)}
+        idx_h, q_h = (binary(index), binary(queries)) if head in BINARY_METRICS else (index, queries)
+        rate, q, cores, dt, ref = cpu_reference_rate(idx_h, q_h, head,
+                                                     sample=wl.get("ref_queries", args.ref_queries),
+                                                     budget_s=args.ref_budget, k=k if knn else None)
+        cpu = {"value": rate, "unit": "queries/s" if knn else "distances/s", "cores": cores, "kind": "port",
+               "sample": f"{q} queries x {index.n_rows} index rows ({dt:.1f}s, oracle numpy port, fp64)"}
+        step(head)
+        if knn:
+            cpu["gpu_topk_index_agreement"] = float((oi[:q].cpu().numpy() == ref[1]).mean())
+        else:
+            got = out[:q, :n].double().cpu().numpy()
+            cpu["gpu_rows_vs_port_max_abs_err"] = float(np.max(np.abs(np.where(ref >= 1e308, 0, got - ref))))
 
     if rank == 0:
         line = {
-            "metric": "pairwise distances/sec", "value": value, "unit": "distances/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if tdt == torch.float32 else "f64",
-            "data": "synthetic (reference generator: zipf s=1.544 degrees, uniform columns, uniform01 values "
-                    "rounded to fp32)",
-            "config": {"workload": f"{args.metric} pairwise distances, {m} query rows per GPU vs the full "
-                                   f"{n} x {index.n_cols} MovieLens-25M-shaped power-law index "
-                                   f"(mean {index.nnz / n:.1f} nnz/row), BASELINE configs[1]",
-                       "metric": args.metric, "queries_per_gpu": m, "index_rows": n, "n_cols": index.n_cols,
-                       "index_nnz": index.nnz, "query_nnz": queries.nnz,
-                       "query_mean_degree": float(qdeg.mean()), "parallelism": f"query-row shards x{world}",
-                       "l2": "inputs + 6.5 GB output per step exceed the 126 MB L2 (no flush needed)",
+            "metric": "kNN queries/sec" if knn else "pairwise distances/sec", "value": value,
+            "unit": "queries/s" if knn else "distances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if knn else "weak", "vs_baseline": None,
+            "dtype": "f32" if tdt == torch.float32 else "f64",
+            "data": "synthetic (reference generator, values rounded to fp32)",
+            "config": {"workload": f"{args.workload}: {head}, {m} query rows vs the full {index_full_rows} x "
+                                   f"{index.n_cols} index ({'k=%d, index rows sharded' % k if knn else 'queries sharded'}"
+                                   f" over {world} GPU(s)); {wl['desc']}",
+                       "metric": head, "queries": m, "index_rows": index_full_rows, "n_cols": index.n_cols,
+                       "index_nnz_per_rank": index.nnz, "query_nnz": queries.nnz,
+                       "parallelism": (f"index-row shards x{world}" if knn else f"query-row shards x{world}"),
+                       "l2": ("inputs + outputs exceed the 126 MB L2 (no flush needed)" if args.workload != "c1" else
+                              "C1 is L2-resident (6 MB inputs, 4 MB output); timed back to back"),
                        "index_build": "once, outside the timed region (cached like the reference's coo_row_ids)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "per_metric": per_metric,
@@ -367,13 +472,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--metric", default="cosine")
-    ap.add_argument("--extra", nargs="*", default=["euclidean", "manhattan"])
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--metric", default=None, help="override the workload's headline metric")
     ap.add_argument("--dtype", choices=["float32", "float64"], default="float32")
-    ap.add_argument("--queries", type=int, default=N_QUERIES)
+    ap.add_argument("--queries", type=int, default=0)
     ap.add_argument("--ref-queries", type=int, default=64)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the workload's secondary metrics")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -7,7 +7,7 @@ import bench
 import paper_2104_06357_b200 as sd
 from paper_2104_06357_b200 import _lib
 
-index, queries = bench.make_data(0, int(os.environ.get("Q", "10000")))
+index, queries = bench.make_data(bench.WORKLOADS[os.environ.get("WL", "c2")], 0, int(os.environ.get("Q", "10000")))
 dev = torch.device("cuda", 0)
 lib = _lib.load()
 res = {}
