@@ -19,17 +19,24 @@ void set_error(const std::string& msg) { g_error = msg; }
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int num_sms() {
-  int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+// device attributes, cached per device (queried on every launch otherwise)
+static int device_attr(cudaDeviceAttr attr, int fallback) {
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> cache[3][kMaxDev];
+  const int slot = attr == cudaDevAttrMultiProcessorCount ? 0
+                 : attr == cudaDevAttrMaxSharedMemoryPerBlockOptin ? 1 : 2;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return fallback;
+  int v = cache[slot][dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, attr, dev) != cudaSuccess || v <= 0) return fallback;
+  cache[slot][dev].store(v, std::memory_order_relaxed);
+  return v;
 }
 
-int64_t smem_optin_bytes() {
-  int dev = 0, v = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  return v > 0 ? v : 227 * 1024;
-}
+int num_sms() { return device_attr(cudaDevAttrMultiProcessorCount, 148); }
+int64_t smem_optin_bytes() { return device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 227 * 1024); }
+int64_t l2_bytes() { return device_attr(cudaDevAttrL2CacheSize, 126 * 1024 * 1024); }
 
 static int check_csr(const sd_csr* m, const char* what) {
   if (!m) { set_error(std::string(what) + " is NULL"); return SD_E_INVALID; }

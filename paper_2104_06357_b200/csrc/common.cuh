@@ -52,6 +52,7 @@ inline cudaStream_t as_stream(sd_stream_t s) { return reinterpret_cast<cudaStrea
 
 int num_sms();
 int64_t smem_optin_bytes();
+int64_t l2_bytes();
 
 // Opt a kernel into `dyn` bytes of dynamic shared memory, accounting for its
 // static shared memory; reports the kernel name on failure.

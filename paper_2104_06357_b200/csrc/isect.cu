@@ -283,11 +283,13 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   const int W = int(std::min<int64_t>(ISECT_MAX_WARPS, (smem_optin_bytes() - 2048) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const int64_t warps = int64_t(num_sms()) * W;
-  // band of tiles whose postings (~100 MB) stay L2-resident while all queries
-  // sweep it; SD_ISECT_BAND overrides (tuning)
+  // bands of tiles whose postings fit the L2 together, so the index streams
+  // from HBM about once while every query sweeps the resident band; bands are
+  // split evenly (no short tail band).  SD_ISECT_BAND overrides (tuning).
   const char* be0 = getenv("SD_ISECT_BAND");
   const int64_t post_bytes = std::max<int64_t>(1, ix->bytes);
-  const int64_t auto_band = (ix->n_tiles * int64_t(100) * 1000 * 1000 + post_bytes - 1) / post_bytes;
+  const int64_t n_bands0 = (post_bytes + l2_bytes() - 1) / l2_bytes();
+  const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
   const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : auto_band));
   const int64_t max_items = m * band0 * ((ix->n_tiles + band0 - 1) / band0);
   Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;

@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
 
     // the first 32 columns of the query and their posting ranges in tile t0;
     // later tiles get theirs prefetched during the previous tile's epilogue
-    const bool valid0 = abeg + lane < aend;
+    // (items of the last, partial band may have an empty tile range: t0 >= t1)
+    const bool valid0 = t0 < t1 && abeg + lane < aend;
     const int32_t c0 = valid0 ? a.a_idx[abeg + lane] : 0;
     const T av0 = valid0 ? a.a_val[abeg + lane] : T(0);
     const uint32_t ar0 = (MX && valid0) ? a.a_rank[abeg + lane] : 255u;

@@ -21,8 +21,11 @@ for tile in [int(t) for t in os.environ.get("TILES", "2048,4096,8192").split(","
     ldo = (n + 3) // 4 * 4
     out = torch.empty((m, ldo), dtype=torch.float32, device=dev)
     flags = _lib.new_flags(dev)
-    for plan in [int(b) for b in os.environ.get("BANDS", "0").split(",")]:
-        os.environ["SD_ISECT_BAND"] = str(plan) if plan else "1000000"
+    for plan in os.environ.get("BANDS", "auto").split(","):   # "auto" = library default, 0 = no bands
+        if plan == "auto":
+            os.environ.pop("SD_ISECT_BAND", None)
+        else:
+            os.environ["SD_ISECT_BAND"] = plan if int(plan) else "1000000"
         for metric in ("cosine", "manhattan"):
             md = _lib.metric_struct(metric)
             ph = (ctypes.c_float * 4)()
@@ -35,6 +38,6 @@ for tile in [int(t) for t in os.environ.get("TILES", "2048,4096,8192").split(","
                 if it:
                     times.append(ph[1])
             res[(tile, plan, metric)] = statistics.median(times)
-            print(f"tile {tile:5d} band {plan} {metric:10s} kernel {statistics.median(times):7.3f} ms", flush=True)
+            print(f"tile {tile:5d} band {plan:>5} {metric:10s} kernel {statistics.median(times):7.3f} ms", flush=True)
     del ix, di
     index_cache = None
