@@ -49,6 +49,11 @@ struct sd_index {
   uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
   void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
   int64_t bytes = 0;
+  // probability that two random postings of one tile belong to the same row
+  // (sum over tiles of sum d_j^2 / sum over tiles of (sum d_j)^2): why packing
+  // several columns into one warp step does not pay on power-law indexes
+  //
+  double collide = 0.0;
 };
 
 namespace sd {
@@ -68,6 +73,15 @@ __global__ void index_count_kernel(const int64_t* __restrict__ ptr, const int32_
   for (int64_t r = warp; r < n_rows; r += nw) {
     const int64_t base = (r / tile) * n_cols;
     for (int64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) atomicAdd(&counts[base + idx[e]], 1u);
+  }
+}
+
+// per-tile sums of row degrees and squared row degrees (collision estimate)
+__global__ void tile_degree_kernel(const int64_t* __restrict__ ptr, int64_t n_rows, int tile, double* sums) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows; r += int64_t(gridDim.x) * blockDim.x) {
+    const double d = double(ptr[r + 1] - ptr[r]);
+    atomicAdd(&sums[2 * (r / tile)], d);
+    atomicAdd(&sums[2 * (r / tile) + 1], d * d);
   }
 }
 
@@ -145,6 +159,24 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
       return SD_OK;
     });
     if (rc != SD_OK) return fail(rc);
+  }
+  if (b->n_rows > 0 && b->nnz > 0) {  // collision estimate (one small D2H at build time)
+    Scratch sums;
+    if (sums.alloc(sizeof(double) * 2 * n_tiles, st) != SD_OK) return fail(SD_E_CUDA);
+    if (cudaMemsetAsync(sums.ptr, 0, sizeof(double) * 2 * n_tiles, st) != cudaSuccess) return fail(SD_E_CUDA);
+    tile_degree_kernel<<<int(std::min<int64_t>((b->n_rows + 255) / 256, 4096)), 256, 0, st>>>(
+        b->indptr, b->n_rows, tile, sums.as<double>());
+    count_launch();
+    std::vector<double> h(2 * n_tiles);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(h.data(), sums.ptr, sizeof(double) * 2 * n_tiles, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("index collision estimate failed");
+      return fail(SD_E_CUDA);
+    }
+    double sq = 0.0, dd = 0.0;
+    for (int64_t t = 0; t < n_tiles; ++t) { dd += h[2 * t] * h[2 * t]; sq += h[2 * t + 1]; }
+    ix->collide = dd > 0.0 ? sq / dd : 0.0;
   }
   *out = ix;
   return SD_OK;

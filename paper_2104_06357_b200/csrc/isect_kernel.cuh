@@ -271,6 +271,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
       uint32_t f = 0;
       zero_val = expand_cell_t<M, T>(T(0), ra0, ra1, T(1), T(1), a.k, a.p, f);
     }
+    // cosine reads the index-row norms only to resolve an empty query row
+    const bool need_sb0 = M != SD_M_COSINE || !(ra0 > T(0));
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
     if constexpr (KPL > 0) top.init();
 
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
           lds4(acc_s + q * ES, gv);
           sts4_zero(acc_s + q * ES, T(0));
           if constexpr (KL) { lds4(cnt_s + q * ES, gcv); sts4_zero(cnt_s + q * ES, T(0)); }
-          if constexpr (SB0) V4<T>::load(a.sb0 + j0 + q, gb0);
+          if constexpr (SB0) { if (need_sb0) V4<T>::load(a.sb0 + j0 + q, gb0); }
           if constexpr (SB1) V4<T>::load(a.sb1 + j0 + q, gb1);
         } else {
 #pragma unroll
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               gv[u] = lds(acc_s + (q + u) * ES, T(0));
               sts(acc_s + (q + u) * ES, T(0));
               if constexpr (KL) { gcv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
-              if constexpr (SB0) gb0[u] = a.sb0[j0 + q + u];
+              if constexpr (SB0) { if (need_sb0) gb0[u] = a.sb0[j0 + q + u]; }
               if constexpr (SB1) gb1[u] = a.sb1[j0 + q + u];
             }
           }
