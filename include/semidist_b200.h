@@ -176,6 +176,9 @@ SD_API int sd_index_build(const sd_csr* b, int dtype, int tile_rows, sd_index** 
 SD_API int sd_index_free(sd_index* index);
 SD_API int64_t sd_index_bytes(const sd_index* index);
 SD_API int sd_index_tile_rows(const sd_index* index);
+/* Index rows held densely for the hybrid path (heavy query rows of dot-family
+ * metrics, hybrid.cu); 0 when the index has no heavy-row block. */
+SD_API int64_t sd_index_heavy_rows(const sd_index* index);
 
 /* Full distance matrix for one catalog metric (pairwise_distances,
  * metrics.py:320-381): out[i*ldo + j] for i < a.n_rows, j < b.n_rows.

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("sd_index_free", _I, [_P]),
     ("sd_index_bytes", _I64, [_P]),
     ("sd_index_tile_rows", _I, [_P]),
+    ("sd_index_heavy_rows", _I64, [_P]),
     ("sd_pairwise", _I, [_CSR, _CSR, _P, _I, ctypes.POINTER(SdMetricDesc), ctypes.POINTER(SdStrategy),
                          _P, _I64, _P, ctypes.POINTER(SdReport), ctypes.POINTER(ctypes.c_float), _P]),
     ("sd_expand", _I, [_P, _I64, _I64, _I64, _I, ctypes.POINTER(SdMetricDesc), _I64,
@@ -217,6 +218,7 @@ class DeviceIndex:
         self.n_rows = dcsr.n_rows
         self.bytes = int(lib.sd_index_bytes(handle))
         self.tile_rows = int(lib.sd_index_tile_rows(handle))
+        self.heavy_rows = int(lib.sd_index_heavy_rows(handle))
 
     def __del__(self):
         try:

@@ -29,6 +29,16 @@ static int device_attr(cudaDeviceAttr attr, int fallback) {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return fallback;
   int v = cache[slot][dev].load(std::memory_order_relaxed);
   if (v > 0) return v;
+  if (slot == 0) {
+    // scratch comes from the device's default stream-ordered pool: keep freed
+    // blocks in the pool across synchronisations instead of returning them to
+    // the driver (each call's large scratch would otherwise be re-mapped)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (cudaDeviceGetAttribute(&v, attr, dev) != cudaSuccess || v <= 0) return fallback;
   cache[slot][dev].store(v, std::memory_order_relaxed);
   return v;

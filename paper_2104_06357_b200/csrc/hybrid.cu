@@ -1,0 +1,326 @@
+// hybrid.cu — dense path for heavy query rows (dot-family metrics).
+//
+// On power-law data a few query rows carry most of the query nonzeros (C2:
+// the 0.8% of queries with >= n_cols/16 nonzeros hold 74% of them) and a few
+// index rows most of the index nonzeros.  In the intersection sweep a query
+// costs one warp step per (query column, index tile) pair, so those heavy
+// queries dominate the sweep although they are a handful of output rows.
+// Their rows are computed densely instead:
+//
+//   heavy queries x heavy index rows   GEMM   HQT^T[nhq x K] * HT[K x n_heavy]
+//   heavy queries x light index rows   gather DLH[j][q] = sum_c b_jc * HQT[c][q]
+//
+// where HT (index build, cached) and HQT (per call) are the dense, column-
+// major (K-major) images of the heavy rows.  heavy_rows_kernel
+// (isect_kernel.cuh) then applies the metric epilogue to those rows; the
+// sweep handles every other query row.  Only metrics whose contribution is a
+// product (semiring.py:76-78) take this path: their dense sums equal the
+// sparse intersection sums up to rounding (products with an absent entry are
+// exact zeros).
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+#include "index.cuh"
+#include "isect_kernel.cuh"
+#include "hybrid.cuh"
+
+namespace sd {
+
+namespace {
+
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+
+}  // namespace
+
+int64_t hybrid_threshold(int64_t n_cols) {
+  return std::max<int64_t>(64, env_i64("SD_HEAVY_DEG", (n_cols + 15) / 16));
+}
+
+// SD_HYBRID: 0 off, 1 automatic (default), 2 forced even for small indexes (tests)
+bool hybrid_enabled() { return env_i64("SD_HYBRID", 1) != 0; }
+bool hybrid_forced() { return env_i64("SD_HYBRID", 1) == 2; }
+
+// ---------------------------------------------------------------- index side
+
+template <typename T>
+__global__ void ht_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                  const T* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                                  int64_t pad, T* __restrict__ dense) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t h = warp; h < nrows; h += nw) {
+    const int64_t r = rows[h];
+    for (int64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) dense[int64_t(idx[e]) * pad + h] = val[e];
+  }
+}
+
+int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st) {
+  if (!hybrid_enabled() || b->n_rows == 0 || b->nnz == 0) return SD_OK;
+  const int64_t theta = hybrid_threshold(b->n_cols);
+  std::vector<int64_t> ptr(b->n_rows + 1);
+  SD_CUDA_TRY(cudaMemcpyAsync(ptr.data(), b->indptr, sizeof(int64_t) * (b->n_rows + 1), cudaMemcpyDeviceToHost, st));
+  SD_CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<int32_t> hid(b->n_rows, -1), rows, light;
+  for (int64_t r = 0; r < b->n_rows; ++r) {
+    if (ptr[r + 1] - ptr[r] >= theta) { hid[r] = int32_t(rows.size()); rows.push_back(int32_t(r)); }
+    else light.push_back(int32_t(r));
+  }
+  // light rows by descending degree: the dense gather takes the long ones first
+  std::stable_sort(light.begin(), light.end(),
+                   [&](int32_t x, int32_t y) { return ptr[x + 1] - ptr[x] > ptr[y + 1] - ptr[y]; });
+  const int64_t nh = int64_t(rows.size());
+  if (nh < 32) return SD_OK;  // nothing worth a dense block
+  const int64_t pad = (nh + 127) / 128 * 128;
+  const size_t es = dtype == SD_F64 ? 8 : 4;
+  const int64_t dense_bytes = b->n_cols * pad * int64_t(es);
+  if (dense_bytes > env_i64("SD_HYBRID_MAX_MB", 1024) << 20) return SD_OK;
+  Scratch drows;
+  SD_TRY(drows.alloc(sizeof(int32_t) * nh, st));
+  if (cudaMalloc(&ix->hid, sizeof(int32_t) * b->n_rows) != cudaSuccess || cudaMalloc(&ix->ht, dense_bytes) != cudaSuccess ||
+      cudaMalloc(&ix->lrows, sizeof(int32_t) * std::max<size_t>(1, light.size())) != cudaSuccess) {
+    set_error("cudaMalloc failed for the hybrid index");
+    return SD_E_CUDA;
+  }
+  SD_CUDA_TRY(cudaMemcpyAsync(ix->hid, hid.data(), sizeof(int32_t) * b->n_rows, cudaMemcpyHostToDevice, st));
+  SD_CUDA_TRY(cudaMemcpyAsync(drows.ptr, rows.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice, st));
+  if (!light.empty())
+    SD_CUDA_TRY(cudaMemcpyAsync(ix->lrows, light.data(), sizeof(int32_t) * light.size(), cudaMemcpyHostToDevice, st));
+  SD_CUDA_TRY(cudaMemsetAsync(ix->ht, 0, dense_bytes, st));
+  const int blocks = int(std::min<int64_t>((nh * 32 + 255) / 256, int64_t(num_sms()) * 8));
+  SD_TRY(SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    ht_scatter_kernel<T><<<blocks, 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
+                                                  drows.as<int32_t>(), nh, pad, static_cast<T*>(ix->ht));
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  }));
+  SD_CUDA_TRY(cudaStreamSynchronize(st));  // the host copies above must outlive the transfers
+  ix->heavy_deg = theta;
+  ix->n_heavy = nh;
+  ix->hpad = pad;
+  ix->n_light = int64_t(light.size());
+  ix->bytes += dense_bytes + int64_t(sizeof(int32_t)) * (b->n_rows + ix->n_light);
+  return SD_OK;
+}
+
+void hybrid_index_free(sd_index* ix) {
+  if (ix->hid) cudaFree(ix->hid);
+  if (ix->ht) cudaFree(ix->ht);
+  if (ix->lrows) cudaFree(ix->lrows);
+  ix->hid = nullptr;
+  ix->ht = nullptr;
+  ix->lrows = nullptr;
+}
+
+// ---------------------------------------------------------------- query side
+
+// heavy query rows get ids 0..cap-1 (the id order is irrelevant to results:
+// every heavy row is computed independently of its slot)
+__global__ void classify_kernel(const int64_t* __restrict__ ptr, int64_t m, int64_t theta, int cap,
+                                int32_t* __restrict__ qid, int32_t* __restrict__ hq, unsigned int* count) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < m; r += int64_t(gridDim.x) * blockDim.x) {
+    int32_t id = -1;
+    if (ptr[r + 1] - ptr[r] >= theta) {
+      const unsigned int k = atomicAdd(count, 1u);
+      if (k < unsigned(cap)) { id = int32_t(k); hq[k] = int32_t(r); }
+    }
+    qid[r] = id;
+  }
+}
+
+// GEMM D = A^T B with A = HQT [K][lda] (heavy queries), B = HT [K][ldb] (heavy
+// index rows), both K-major.  CTA tile 32 x 128, 128 threads with 4 x 8
+// accumulators each (operands read from shared memory as 16-byte vectors), K
+// split across blockIdx.z into partial tiles that hreduce_kernel sums in
+// split order (deterministic).
+constexpr int HG_BM = 32, HG_BN = 128, HG_BK = 16, HG_THREADS = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__ A, const T* __restrict__ B, int64_t K,
+                                                           int64_t lda, int64_t ldb, int64_t kchunk, int64_t ldp,
+                                                           int64_t rows, T* __restrict__ P) {
+  __shared__ __align__(16) T As[2][HG_BK][HG_BM];
+  __shared__ __align__(16) T Bs[2][HG_BK][HG_BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t q0 = int64_t(blockIdx.y) * HG_BM, h0 = int64_t(blockIdx.x) * HG_BN;
+  const int64_t kb = int64_t(blockIdx.z) * kchunk, ke = tmin<int64_t>(K, kb + kchunk);
+  // global -> register staging: A tile 16 x 32 (4 per thread), B tile 16 x 128 (16 per thread)
+  const int sr = tid >> 3, ac = (tid & 7) * 4, bc = (tid & 7) * 16;
+  T ra[4], rb[16];
+  auto gload = [&](int64_t k0) {
+    const int64_t k = k0 + sr;
+    if (k < ke) {
+      V4<T>::load(A + k * lda + q0 + ac, ra);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) V4<T>::load(B + k * ldb + h0 + bc + 4 * v, rb + 4 * v);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ra[u] = T(0);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) rb[u] = T(0);
+    }
+  };
+  auto sstore = [&](int buf) {
+    V4<T>::store_plain(&As[buf][sr][ac], ra);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) V4<T>::store_plain(&Bs[buf][sr][bc + 4 * v], rb + 4 * v);
+  };
+  T acc[4][8];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y] = T(0);
+  gload(kb);
+  sstore(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = kb; k0 < ke; k0 += HG_BK) {
+    const bool more = k0 + HG_BK < ke;
+    if (more) gload(k0 + HG_BK);
+#pragma unroll
+    for (int kk = 0; kk < HG_BK; ++kk) {
+      T a[4], b[8];
+      V4<T>::load(&As[buf][kk][ty * 4], a);
+      V4<T>::load(&Bs[buf][kk][tx * 4], b);
+      V4<T>::load(&Bs[buf][kk][64 + tx * 4], b + 4);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y] = fma_rn(a[x], b[y], acc[x][y]);
+    }
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  T* out = P + int64_t(blockIdx.z) * rows * ldp;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    T* row = out + (q0 + ty * 4 + x) * ldp + h0;
+    V4<T>::store_plain(row + tx * 4, acc[x]);
+    V4<T>::store_plain(row + 64 + tx * 4, acc[x] + 4);
+  }
+}
+
+template <typename T>
+__global__ void hreduce_kernel(const T* __restrict__ P, int splits, int64_t count, T* __restrict__ D) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
+    T s = P[e];
+    for (int z = 1; z < splits; ++z) s = add_rn(s, P[int64_t(z) * count + e]);
+    D[e] = s;
+  }
+}
+
+// DLH[j][q] = sum_c b_jc * HQT[c][q] over light index rows j (heavy rows are
+// the GEMM's); one warp per (row, 128-wide block of heavy queries), ascending
+// column order, 8 dense rows in flight per lane.  Rows are taken from a
+// shared counter in descending-degree order (lrows, index build) so the long
+// rows start first and no warp is left with a tail of them.
+template <typename T>
+__global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                                      const T* __restrict__ val, const int32_t* __restrict__ lrows,
+                                                      int64_t n_light, const T* __restrict__ D, int64_t ld,
+                                                      int64_t nblk, unsigned long long* counter, T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long total = (unsigned long long)(n_light * nblk);
+  while (true) {
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(counter, 1ull);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= total) break;
+    const int64_t j = lrows[it / nblk], blk = int64_t(it % nblk);
+    const int64_t beg = ptr[j], end = ptr[j + 1];
+    const T* dcol = D + blk * 128 + 4 * lane;
+    T acc[4] = {T(0), T(0), T(0), T(0)};
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+      const bool ok = e0 + lane < end;
+      const int32_t cl = ok ? idx[e0 + lane] : 0;
+      const T vl = ok ? val[e0 + lane] : T(0);
+      const int nn = int(tmin<int64_t>(32, end - e0));
+      for (int u0 = 0; u0 < nn; u0 += 8) {
+        T d[8][4];
+        T x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int src = (u0 + u) & 31;
+          const int32_t c = __shfl_sync(0xffffffffu, cl, src);
+          x[u] = __shfl_sync(0xffffffffu, vl, src);
+          if (u0 + u < nn) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u0 + u < nn)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = fma_rn(x[u], d[u][k], acc[k]);
+      }
+    }
+    V4<T>::store_plain(out + j * ld + blk * 128 + 4 * lane, acc);
+  }
+}
+
+// ---------------------------------------------------------------- driver
+
+int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, HybridState& hs,
+                   cudaStream_t st) {
+  hs.nhq = 0;
+  const int64_t m = a->n_rows;
+  const int cap = int(env_i64("SD_HYBRID_MAX_QUERIES", 1024));
+  SD_TRY(hs.qid.alloc(sizeof(int32_t) * std::max<int64_t>(1, m), st));
+  SD_TRY(hs.hq.alloc(sizeof(int32_t) * cap, st));
+  SD_TRY(hs.count.alloc(sizeof(unsigned int), st));
+  SD_CUDA_TRY(cudaMemsetAsync(hs.count.ptr, 0, sizeof(unsigned int), st));
+  SD_TRY(hs.gcount.alloc(sizeof(unsigned long long), st));
+  SD_CUDA_TRY(cudaMemsetAsync(hs.gcount.ptr, 0, sizeof(unsigned long long), st));
+  const int blocks = int(std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 8));
+  classify_kernel<<<std::max(1, blocks), 256, 0, st>>>(a->indptr, m, ix->heavy_deg, cap, hs.qid.as<int32_t>(),
+                                                       hs.hq.as<int32_t>(), hs.count.as<unsigned int>());
+  SD_LAUNCH_CHECK();
+  unsigned int cnt = 0;
+  SD_CUDA_TRY(cudaMemcpyAsync(&cnt, hs.count.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+  SD_CUDA_TRY(cudaStreamSynchronize(st));
+  hs.nhq = int(std::min<unsigned int>(cnt, unsigned(cap)));
+  if (hs.nhq == 0) return SD_OK;
+  const size_t es = dtype == SD_F64 ? 8 : 4;
+  const int64_t K = a->n_cols;
+  hs.qpad = (hs.nhq + 127) / 128 * 128;
+  SD_TRY(hs.hqt.alloc(es * size_t(K) * size_t(hs.qpad), st));
+  SD_CUDA_TRY(cudaMemsetAsync(hs.hqt.ptr, 0, es * size_t(K) * size_t(hs.qpad), st));
+  const int64_t tiles_q = (hs.nhq + HG_BM - 1) / HG_BM, tiles_h = ix->hpad / HG_BN;
+  const int64_t rows = tiles_q * HG_BM;  // GEMM rows computed (<= qpad)
+  // K split so that the GEMM fills about three waves of CTAs
+  const int64_t want = std::max<int64_t>(1, (3 * 2 * int64_t(num_sms()) + tiles_q * tiles_h - 1) / (tiles_q * tiles_h));
+  int64_t kchunk = (K + want - 1) / want;
+  kchunk = std::max<int64_t>(HG_BK, (kchunk + HG_BK - 1) / HG_BK * HG_BK);
+  const int64_t splits = (K + kchunk - 1) / kchunk;
+  SD_TRY(hs.part.alloc(es * size_t(splits) * size_t(rows) * size_t(ix->hpad), st));
+  SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
+  SD_TRY(hs.dlh.alloc(es * size_t(std::max<int64_t>(1, b->n_rows)) * size_t(hs.qpad), st));
+  const int gblocks = int(std::min<int64_t>((int64_t(hs.nhq) * 32 + 255) / 256, int64_t(num_sms()) * 8));
+  return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    ht_scatter_kernel<T><<<gblocks, 256, 0, st>>>(a->indptr, a->indices, static_cast<const T*>(a->values),
+                                                  hs.hq.as<int32_t>(), hs.nhq, hs.qpad, hs.hqt.as<T>());
+    SD_LAUNCH_CHECK();
+    hgemm_kernel<T><<<dim3(unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)), HG_THREADS, 0, st>>>(
+        hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad, ix->hpad, kchunk, ix->hpad, rows,
+        hs.part.as<T>());
+    SD_LAUNCH_CHECK();
+    const int64_t count = rows * ix->hpad;
+    hreduce_kernel<T><<<int(std::min<int64_t>((count + 255) / 256, int64_t(num_sms()) * 16)), 256, 0, st>>>(
+        hs.part.as<T>(), int(splits), count, hs.dqh.as<T>());
+    SD_LAUNCH_CHECK();
+    const int64_t nblk = hs.qpad / 128;
+    int per_sm = 0;
+    SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T>, 256, 0));
+    hgather_kernel<T><<<std::max(1, per_sm) * num_sms(), 256, 0, st>>>(
+        b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hs.qpad,
+        nblk, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  });
+}
+
+}  // namespace sd

@@ -1,0 +1,29 @@
+// hybrid.cuh — per-call state of the dense path for heavy query rows (hybrid.cu).
+#pragma once
+#include "common.cuh"
+
+struct sd_index;
+
+namespace sd {
+
+struct HybridState {
+  int nhq = 0;          // heavy query rows of this call (ids 0..nhq-1)
+  int64_t qpad = 0;     // nhq rounded up to 128
+  Scratch qid;          // [m] heavy id of each query row or -1
+  Scratch hq;           // [cap] query row of each heavy id
+  Scratch count;
+  Scratch gcount;       // work counter of the dense gather
+  Scratch hqt;          // [n_cols][qpad] dense heavy query rows
+  Scratch part;         // GEMM K-split partials
+  Scratch dqh;          // [qpad][hpad] heavy query x heavy index row sums
+  Scratch dlh;          // [n][qpad] light index row x heavy query sums
+};
+
+int64_t hybrid_threshold(int64_t n_cols);
+bool hybrid_enabled();
+bool hybrid_forced();
+// classify query rows, then GEMM + gather for the heavy ones (no-op when none)
+int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, HybridState& hs,
+                   cudaStream_t st);
+
+}  // namespace sd

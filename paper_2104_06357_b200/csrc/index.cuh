@@ -1,0 +1,46 @@
+// index.cuh — the J-blocked inverted index of B (isect.cu) and its dense
+// heavy-row block for the hybrid path (hybrid.cu).
+#pragma once
+#include <mutex>
+#include <vector>
+#include "common.cuh"
+#include "prep.cuh"
+
+struct sd_index {
+  // per-row statistics of the index rows, computed once per (metric, p) and
+  // owned by the index (they are a property of B, like the postings)
+  struct StatEntry {
+    int metric;
+    double p;
+    void* buf;
+    sd::Stats stats;
+  };
+  std::mutex mu;
+  std::vector<StatEntry> stat_cache;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int tile = 0;
+  int64_t n_tiles = 0;
+  int dtype = 0;
+  uint32_t* colptr = nullptr;  // [n_tiles * n_cols + 1]
+  void* post = nullptr;        // [nnz] Posting<T> (row id within tile, value)
+  uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
+  void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
+  int64_t bytes = 0;
+  // probability that two random postings of one tile belong to the same row
+  // (sum over tiles of sum d_j^2 / sum over tiles of (sum d_j)^2): why packing
+  // several columns into one warp step does not pay on power-law indexes
+  //
+  double collide = 0.0;
+  // hybrid path (hybrid.cu): rows of degree >= heavy_deg, densely as HT
+  int64_t heavy_deg = 0, n_heavy = 0, hpad = 0;
+  int32_t* hid = nullptr;  // [n_rows]: heavy id or -1
+  void* ht = nullptr;      // [n_cols][hpad] T: HT[c][h] = B[heavy row h][c]
+  int32_t* lrows = nullptr;  // [n_light] the other rows, by descending degree
+  int64_t n_light = 0;
+};
+
+namespace sd {
+// hybrid.cu
+int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st);
+void hybrid_index_free(sd_index* ix);
+}  // namespace sd

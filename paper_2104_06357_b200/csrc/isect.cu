@@ -29,32 +29,8 @@
 #include "topk.cuh"
 #include "isect_kernel.cuh"
 
-struct sd_index {
-  // per-row statistics of the index rows, computed once per (metric, p) and
-  // owned by the index (they are a property of B, like the postings)
-  struct StatEntry {
-    int metric;
-    double p;
-    void* buf;
-    sd::Stats stats;
-  };
-  std::mutex mu;
-  std::vector<StatEntry> stat_cache;
-  int64_t n_rows = 0, n_cols = 0, nnz = 0;
-  int tile = 0;
-  int64_t n_tiles = 0;
-  int dtype = 0;
-  uint32_t* colptr = nullptr;  // [n_tiles * n_cols + 1]
-  void* post = nullptr;        // [nnz] Posting<T> (row id within tile, value)
-  uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
-  void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
-  int64_t bytes = 0;
-  // probability that two random postings of one tile belong to the same row
-  // (sum over tiles of sum d_j^2 / sum over tiles of (sum d_j)^2): why packing
-  // several columns into one warp step does not pay on power-law indexes
-  //
-  double collide = 0.0;
-};
+#include "index.cuh"
+#include "hybrid.cuh"
 
 namespace sd {
 
@@ -178,6 +154,10 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
     for (int64_t t = 0; t < n_tiles; ++t) { dd += h[2 * t] * h[2 * t]; sq += h[2 * t + 1]; }
     ix->collide = dd > 0.0 ? sq / dd : 0.0;
   }
+  {
+    const int rc = hybrid_index_build(b, dtype, ix, st);
+    if (rc != SD_OK) return fail(rc);
+  }
   *out = ix;
   return SD_OK;
 }
@@ -188,6 +168,7 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
 // degree 25k is spread over up to n_tiles warps instead of serialising on one.
 __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ ptr, int64_t m, int64_t n_tiles,
                                                     int64_t band, int64_t warps, int64_t epi_cost, int tile_major,
+                                                    const int32_t* __restrict__ skip,
                                                     int32_t* __restrict__ order, int32_t* __restrict__ tpi,
                                                     int64_t* __restrict__ item_off, int32_t* __restrict__ item_pos) {
   __shared__ unsigned int hist[64];
@@ -202,7 +183,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     const int64_t d = ptr[r + 1] - ptr[r];
     const int b = d > 0 ? 63 - __clzll(d) : 0;
     atomicAdd(&hist[63 - b], 1u);
-    local += (unsigned long long)(d + epi_cost);
+    if (!skip || skip[r] < 0) local += (unsigned long long)(d + epi_cost);
   }
   atomicAdd(&total, local);
   __syncthreads();
@@ -233,7 +214,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     const int64_t cost = ptr[r + 1] - ptr[r] + epi_cost;
     const int64_t t = tmin<int64_t>(band, tmax<int64_t>(1, target / cost));
     tpi[q] = int32_t(t);
-    sum += (band + t - 1) / t;
+    if (!skip || skip[r] < 0) sum += (band + t - 1) / t;  // rows of the hybrid path get no items
   }
   part[threadIdx.x] = sum;
   __syncthreads();
@@ -246,7 +227,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
   int64_t off = part[threadIdx.x];
   for (int64_t q = lo; q < hi; ++q) {
     item_off[q] = off;
-    const int64_t cnt = (band + tpi[q] - 1) / tpi[q];
+    const int64_t cnt = (skip && skip[order[q]] >= 0) ? 0 : (band + tpi[q] - 1) / tpi[q];
     for (int64_t it = 0; it < cnt; ++it) item_pos[off + it] = int32_t(q);
     off += cnt;
   }
@@ -334,7 +315,14 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
   const int tile_major = pe ? atoi(pe) : 0;
   const int64_t band = band0;
+  // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
+  // computed densely; the sweep skips them
+  HybridState hs;
+  if (topk == 0 && ck == C_MUL && !tile_major && ix->n_heavy > 0 && hybrid_enabled() &&
+      (ix->n_tiles >= 4 || hybrid_forced()))  // small indexes: the sweep is cheap, keep it exact
+    SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
   plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
+                                  hs.nhq > 0 ? hs.qid.as<int32_t>() : nullptr,
                                   order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
                                   item_pos.as<int32_t>());
   SD_LAUNCH_CHECK();
@@ -354,6 +342,8 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.item_off = item_off.as<int64_t>(); args.item_pos = item_pos.as<int32_t>();
     args.counter = counter.as<unsigned int>();
     args.tile_major = tile_major;
+    const char* de = getenv("SD_ISECT_DEBUG");
+    args.debug = de ? atoi(de) : 0;
     args.band = band;
     args.strict = md->strict;
     args.k = T(a->n_cols); args.p = T(md->p);
@@ -366,6 +356,9 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.topb = static_cast<const T*>(ix->topb);
     args.b_ptr = b->indptr; args.b_idx = b->indices; args.b_val = static_cast<const T*>(b->values);
     SD_TRY(isect_launch(args, md->metric, W, st));
+    if (hs.nhq > 0)
+      SD_TRY(isect_heavy_rows(args, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(), ix->hpad,
+                              hs.dlh.as<T>(), hs.qpad, st));
     if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
     return SD_OK;
   });
@@ -380,9 +373,11 @@ int sd_index_free(sd_index* ix) {
   if (ix->post_rank) cudaFree(ix->post_rank);
   if (ix->topb) cudaFree(ix->topb);
   for (auto& e : ix->stat_cache) cudaFree(e.buf);
+  sd::hybrid_index_free(ix);
   delete ix;
   return SD_OK;
 }
 
 int64_t sd_index_bytes(const sd_index* ix) { return ix ? ix->bytes : 0; }
 int sd_index_tile_rows(const sd_index* ix) { return ix ? ix->tile : 0; }
+int64_t sd_index_heavy_rows(const sd_index* ix) { return ix ? ix->n_heavy : 0; }

@@ -2,6 +2,7 @@
 // Templated on <value type, metric, top-k slots per lane>; instantiations live
 // in isect_f32.cu / isect_f64.cu so they compile in parallel.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 #include "metric.cuh"
 #include "prep.cuh"
@@ -33,6 +34,7 @@ struct IsectArgs {
   const int32_t* item_pos;  // item -> plan position
   unsigned int* counter;
   int tile_major;           // items are (tile, position) pairs in tile-major order
+  int debug;                // timing experiments (SD_ISECT_DEBUG): 1 skip the sweep, 2 skip the epilogue
   int64_t band;             // tiles per band (band-major plan)
   int strict;
   T k, p;
@@ -58,6 +60,12 @@ __device__ __forceinline__ uint32_t to_mask(double v) { return uint32_t(v); }
 __device__ __forceinline__ float from_mask(uint32_t m, float) { return __uint_as_float(m); }
 __device__ __forceinline__ double from_mask(uint32_t m, double) { return double(m); }
 
+// fast epilogue: 128-cell groups in flight per warp
+#ifndef SD_ISECT_EPF
+#define SD_ISECT_EPF 2
+#endif
+constexpr int EPF = SD_ISECT_EPF;
+
 // warps per CTA (one CTA per SM: 14 x 16 KB accumulators = 224 KB); capping
 // the CTA at 448 threads gives each thread up to 144 registers
 constexpr int ISECT_MAX_WARPS = 14;
@@ -78,6 +86,9 @@ template <> struct V4<float> {
   __device__ __forceinline__ static void store(float* p, const float* v) {  // streaming store
     __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
   }
+  __device__ __forceinline__ static void store_plain(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
 };
 template <> struct V4<double> {
   __device__ __forceinline__ static void load(const double* p, double* v) {
@@ -88,6 +99,10 @@ template <> struct V4<double> {
   __device__ __forceinline__ static void store(double* p, const double* v) {
     __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
     __stcs(reinterpret_cast<double2*>(p) + 1, make_double2(v[2], v[3]));
+  }
+  __device__ __forceinline__ static void store_plain(double* p, const double* v) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
   }
 };
 
@@ -180,8 +195,37 @@ __device__ __forceinline__ T fused_value(const IsectArgs<T>& a, T acc, T cnt, T 
   }
 }
 
+// Final value of one cell from its accumulated intersection value gv (and
+// count gcv), the query statistics ra0/ra1 and the index-row statistics
+// gb0/gb1 (every metric except chebyshev).  Shared by the fused epilogue and
+// the heavy-query epilogue so both produce identical bits.
+template <typename T, int M>
+__device__ __forceinline__ T isect_cell(const IsectArgs<T>& a, T gv, T gcv, T ra0, T ra1, T gb0, T gb1,
+                                        bool fast_zero, T zero_val, uint32_t& f) {
+  if constexpr (M == SD_M_COSINE) {
+    if (ra0 > T(0)) return sub_rn(T(1), mul_rn(gv, mul_rn(ra1, gb1)));  // gb1 = 1/||b|| (0 if empty)
+    return gb0 == T(0) ? T(0) : T(1);  // empty query row (metrics.py:116-118): 0 against empty rows, else 1
+  } else {
+    if (fast_zero && gv == T(0)) return zero_val;
+    return fused_value<T, M>(a, gv, gcv, ra0, ra1, gb0, gb1, f);
+  }
+}
+
+// per-query constants of isect_cell: cells without intersections of a
+// non-empty query row take zero_val without the division
+template <typename T, int M>
+__device__ __forceinline__ void isect_zero(const IsectArgs<T>& a, T ra0, T ra1, bool& fast_zero, T& zero_val) {
+  fast_zero = false;
+  zero_val = T(0);
+  if constexpr (sparse_result<M>()) {
+    fast_zero = (M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_JACCARD) ? ra0 > T(0) : true;
+    uint32_t f = 0;
+    zero_val = expand_cell_t<M, T>(T(0), ra0, ra1, T(1), T(1), a.k, a.p, f);
+  }
+}
+
 template <typename T, int M, int KPL>
-__global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const IsectArgs<T> a) {
+__global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const IsectArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CK = metric_contrib(M);
   constexpr bool MX = CK == C_MAX;
@@ -264,13 +308,9 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
     T topa_l = T(0);  // chebyshev: lane r holds the r-th largest |a| of the query row
     if constexpr (MX) topa_l = lane < CHEB_K ? a.topa[int64_t(lane) * a.m + i] : T(0);
     // value of a cell without intersections when the query row is non-empty
-    bool fast_zero = false;
-    T zero_val = T(0);
-    if constexpr (sparse_result<M>()) {
-      fast_zero = (M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_JACCARD) ? ra0 > T(0) : true;
-      uint32_t f = 0;
-      zero_val = expand_cell_t<M, T>(T(0), ra0, ra1, T(1), T(1), a.k, a.p, f);
-    }
+    bool fast_zero;
+    T zero_val;
+    isect_zero<T, M>(a, ra0, ra1, fast_zero, zero_val);
     // cosine reads the index-row norms only to resolve an empty query row
     const bool need_sb0 = M != SD_M_COSINE || !(ra0 > T(0));
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
@@ -297,7 +337,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
       uint32_t ar = ar0;
       uint32_t pb = pb0;
       uint32_t pe = pe0;
-      for (int64_t base = abeg; base < aend; base += 32) {
+      for (int64_t base = (a.debug & 1) ? aend : abeg; base < aend; base += 32) {
         const int ncol = int(tmin<int64_t>(32, aend - base));
         const uint32_t cur_pb = pb;
         const T cur_av = av;
@@ -378,6 +418,62 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
         pb0 = valid0 ? cp[a.n_cols + c0] : 0u;
         pe0 = valid0 ? cp[a.n_cols + c0 + 1] : 0u;
       }
+      if (a.debug & 2) continue;
+      if constexpr (KPL == 0 && !MX) {
+        // full tile, 16-byte aligned output rows: a straight-line epilogue with
+        // pointers advanced per group, no bounds tests, and the per-query
+        // cosine branch hoisted out of the cell loop
+        if (vec_out && nt == TJ && TJ % (EPF * 128) == 0) {
+          auto run = [&](auto nz) {
+            constexpr bool NZ = decltype(nz)::value;
+            T* op = a.out + i * a.ldo + j0 + 4 * lane;
+            const T* p0 = SB0 ? a.sb0 + j0 + 4 * lane : nullptr;
+            const T* p1 = SB1 ? a.sb1 + j0 + 4 * lane : nullptr;
+            uint32_t sa = acc_s + 4u * uint32_t(lane) * ES;
+            uint32_t sc = cnt_s + 4u * uint32_t(lane) * ES;
+            // EPF register sets: group g is finished while the next EPF-1
+            // groups' shared and global loads are in flight
+            T gv[EPF][4], gc[EPF][4], g0[EPF][4], g1[EPF][4];
+            auto load = [&](uint32_t off, T* v, T* c, T* b0, T* b1) {
+              lds4(sa + off * ES, v);
+              sts4_zero(sa + off * ES, T(0));
+              if constexpr (KL) { lds4(sc + off * ES, c); sts4_zero(sc + off * ES, T(0)); }
+              if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) V4<T>::load(p0 + off, b0);
+              if constexpr (SB1) V4<T>::load(p1 + off, b1);
+            };
+            auto finish = [&](uint32_t off, const T* v, const T* c, const T* b0, const T* b1) {
+              T r[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if constexpr (M == SD_M_COSINE && NZ) {
+                  r[u] = sub_rn(T(1), mul_rn(v[u], mul_rn(ra1, b1[u])));
+                } else {
+                  uint32_t f = 0;
+                  r[u] = isect_cell<T, M>(a, v[u], KL ? c[u] : T(0), ra0, ra1, SB0 ? b0[u] : T(0),
+                                          SB1 ? b1[u] : T(0), fast_zero, zero_val, f);
+                  flags |= f;
+                }
+              }
+              V4<T>::store(op + off, r);
+            };
+#pragma unroll
+            for (int q = 0; q < EPF; ++q) load(uint32_t(q) * 128u, gv[q], gc[q], g0[q], g1[q]);
+#pragma unroll 1
+            for (uint32_t g = 0; g < uint32_t(TJ); g += EPF * 128) {
+#pragma unroll
+              for (int q = 0; q < EPF; ++q) {
+                finish(g + uint32_t(q) * 128u, gv[q], gc[q], g0[q], g1[q]);
+                if (g + uint32_t(q + EPF) * 128u < uint32_t(TJ))
+                  load(g + uint32_t(q + EPF) * 128u, gv[q], gc[q], g0[q], g1[q]);
+              }
+            }
+          };
+          if (M == SD_M_COSINE && ra0 > T(0)) run(std::true_type{});
+          else run(std::false_type{});
+          __syncwarp();
+          continue;
+        }
+      }
       // epilogue: each lane finishes 4 consecutive cells per step (16-byte
       // shared/global accesses); the accumulator is re-zeroed as it is read
       T* orow = KPL == 0 ? a.out + i * a.ldo + j0 : nullptr;
@@ -445,25 +541,12 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32) isect_kernel(const Isect
               r[u] = mb > x ? mb : x;
             }
           }
-        } else if constexpr (M == SD_M_COSINE) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (ra0 > T(0)) {
-              r[u] = sub_rn(T(1), mul_rn(gv[u], mul_rn(ra1, gb1[u])));   // gb1 = 1/||b|| (0 if empty)
-            } else {  // empty query row (metrics.py:116-118): 0 against empty rows, else 1
-              r[u] = gb0[u] == T(0) ? T(0) : T(1);
-            }
-          }
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if (fast_zero && gv[u] == T(0)) {
-              r[u] = zero_val;
-            } else {
-              uint32_t f = 0;
-              r[u] = fused_value<T, M>(a, gv[u], gcv[u], ra0, ra1, gb0[u], gb1[u], f);
-              if (q + u < nt) flags |= f;  // lanes past the tile end evaluate a dummy cell
-            }
+            uint32_t f = 0;
+            r[u] = isect_cell<T, M>(a, gv[u], gcv[u], ra0, ra1, gb0[u], gb1[u], fast_zero, zero_val, f);
+            if (q + u < nt) flags |= f;  // lanes past the tile end evaluate a dummy cell
           }
         }
         if constexpr (KPL > 0) {
@@ -528,6 +611,76 @@ __global__ void merge_items_kernel(const T* __restrict__ cd, const int64_t* __re
   }
 }
 
+
+// Heavy query rows of the hybrid path (hybrid.cu, dot-family metrics): every
+// cell of such a row comes from the dense path — heavy index rows from dqh
+// ([nhq][hpad], the GEMM), light index rows from dlh ([n][qpad], the dense
+// gather).  A CTA stages JB rows of dlh in shared memory so that both the dlh
+// reads and the output rows stay coalesced.
+template <typename T, int M>
+__global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, const int32_t* __restrict__ hq,
+                                                         int nhq, const int32_t* __restrict__ hid,
+                                                         const T* __restrict__ dqh, int64_t hpad,
+                                                         const T* __restrict__ dlh, int64_t qpad, int JB) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t qs = qpad + 1;  // padded row stride: lanes read one column across rows
+  T* sv = reinterpret_cast<T*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nblk = (a.n + JB - 1) / JB;
+  uint32_t flags = 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t j0 = blk * JB;
+    const int jn = int(tmin<int64_t>(JB, a.n - j0));
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < int64_t(jn) * qpad; e += blockDim.x) {
+      const int64_t jj = e / qpad;
+      sv[jj * qs + (e - jj * qpad)] = dlh[j0 * qpad + e];
+    }
+    __syncthreads();
+    for (int qq = warp; qq < nhq; qq += int(blockDim.x >> 5)) {
+      const int64_t i = hq[qq];
+      const T ra0 = a.sa0 ? a.sa0[i] : T(0);
+      const T ra1 = a.sa1 ? a.sa1[i] : T(0);
+      bool fast_zero;
+      T zero_val;
+      isect_zero<T, M>(a, ra0, ra1, fast_zero, zero_val);
+      for (int jj = lane; jj < jn; jj += 32) {
+        const int64_t j = j0 + jj;
+        const int32_t h = hid[j];
+        const T gv = h >= 0 ? dqh[int64_t(qq) * hpad + h] : sv[jj * qs + qq];
+        const T gb0 = a.sb0 ? a.sb0[j] : T(0);
+        const T gb1 = a.sb1 ? a.sb1[j] : T(0);
+        uint32_t f = 0;
+        __stcs(a.out + i * a.ldo + j, isect_cell<T, M>(a, gv, T(0), ra0, ra1, gb0, gb1, fast_zero, zero_val, f));
+        flags |= f;
+      }
+    }
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (flags && lane == 0) atomicOr(a.flags, flags);
+}
+
+template <typename T, int M>
+int launch_heavy_rows(IsectArgs<T>& a, const int32_t* hq, int nhq, const int32_t* hid, const T* dqh,
+                      int64_t hpad, const T* dlh, int64_t qpad, cudaStream_t st) {
+  if (nhq <= 0) return SD_OK;
+  if constexpr (metric_contrib(M) != C_MUL) {
+    set_error("the hybrid path serves dot-family metrics only");
+    return SD_E_UNSUPPORTED;
+  } else {
+    const int64_t per_row = (qpad + 1) * int64_t(sizeof(T));
+    const int JB = int(tmin<int64_t>(64, (smem_optin_bytes() - 4096) / per_row));
+    if (JB < 1) { set_error("too many heavy query rows for the hybrid epilogue"); return SD_E_INVALID; }
+    const size_t smem = size_t(JB) * size_t(per_row);
+    SD_TRY(prepare_smem(heavy_rows_kernel<T, M>, smem, "heavy_rows_kernel"));
+    const int64_t nblk = (a.n + JB - 1) / JB;
+    const int blocks = int(tmin<int64_t>(nblk, int64_t(num_sms()) * 8));
+    heavy_rows_kernel<T, M><<<blocks, 256, smem, st>>>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, JB);
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  }
+}
+
 template <typename T, int M, int KPL>
 int launch_isect_kernel(IsectArgs<T>& args, int W, cudaStream_t st) {
   const int64_t per_warp = int64_t(args.tile) * sizeof(T) *
@@ -571,6 +724,20 @@ int launch_isect_metric(IsectArgs<T>& args, int W, cudaStream_t st) {
       default: set_error("metric has no fused intersection kernel"); return SD_E_UNSUPPORTED;      \
     }                                                                                               \
   }                                                                                                 \
+  int isect_heavy_rows(IsectArgs<T>& a, int metric, const int32_t* hq, int nhq, const int32_t* hid,                     \
+                       const T* dqh, int64_t hpad, const T* dlh, int64_t qpad, cudaStream_t st) {                       \
+    switch (metric) {                                                                                                   \
+      case SD_M_CORRELATION: return launch_heavy_rows<T, SD_M_CORRELATION>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);  \
+      case SD_M_COSINE: return launch_heavy_rows<T, SD_M_COSINE>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);            \
+      case SD_M_DICE: return launch_heavy_rows<T, SD_M_DICE>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);                \
+      case SD_M_DOT: return launch_heavy_rows<T, SD_M_DOT>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);                  \
+      case SD_M_EUCLIDEAN: return launch_heavy_rows<T, SD_M_EUCLIDEAN>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);      \
+      case SD_M_HELLINGER: return launch_heavy_rows<T, SD_M_HELLINGER>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);      \
+      case SD_M_JACCARD: return launch_heavy_rows<T, SD_M_JACCARD>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);          \
+      case SD_M_RUSSELRAO: return launch_heavy_rows<T, SD_M_RUSSELRAO>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);      \
+      default: set_error("metric has no hybrid path"); return SD_E_UNSUPPORTED;                                         \
+    }                                                                                                                   \
+  }                                                                                                                     \
   int isect_merge(IsectArgs<T>& a, int64_t base, T* od, int64_t* oi, cudaStream_t st) {            \
     const int blocks = int(std::min<int64_t>((a.m * 32 + 255) / 256, int64_t(num_sms()) * 16));    \
     if (a.topk <= 32)                                                                               \
@@ -590,6 +757,10 @@ int launch_isect_metric(IsectArgs<T>& args, int W, cudaStream_t st) {
 int isect_launch(IsectArgs<float>& args, int metric, int W, cudaStream_t st);
 int isect_launch(IsectArgs<double>& args, int metric, int W, cudaStream_t st);
 int isect_merge(IsectArgs<float>& a, int64_t base, float* od, int64_t* oi, cudaStream_t st);
+int isect_heavy_rows(IsectArgs<float>& a, int metric, const int32_t* hq, int nhq, const int32_t* hid,
+                     const float* dqh, int64_t hpad, const float* dlh, int64_t qpad, cudaStream_t st);
+int isect_heavy_rows(IsectArgs<double>& a, int metric, const int32_t* hq, int nhq, const int32_t* hid,
+                     const double* dqh, int64_t hpad, const double* dlh, int64_t qpad, cudaStream_t st);
 int isect_merge(IsectArgs<double>& a, int64_t base, double* od, int64_t* oi, cudaStream_t st);
 
 }  // namespace sd

@@ -365,3 +365,37 @@ def test_tile_bands_partial_and_invariant(dtype, monkeypatch):
     sub = _gather_rows(idx, cols)
     ref = O.pairwise_distances(q, sub, "cosine")
     assert_parity(outs[0][:, cols], ref, q, sub, "cosine", dtype, what="bands sample")
+
+
+DOT_FAMILY = ("cosine", "euclidean", "correlation", "dot", "dice", "jaccard", "hellinger", "russelrao")
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_hybrid_heavy_rows_vs_oracle(dtype, monkeypatch):
+    """Hybrid path (hybrid.cu): query rows with >= n_cols/16 nonzeros are
+    computed densely (GEMM against the index's heavy rows + gather over its
+    light rows) and the sweep skips them.  Every dot-family metric against the
+    oracle, and against the sweep-only path (SD_HYBRID=0) within rounding."""
+    import torch
+    from paper_2104_06357_b200 import _lib
+    idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
+    deg = np.diff(np.asarray(idx.indptr))
+    heavy = np.flatnonzero(deg >= 100)
+    assert len(heavy) >= 64
+    rows = np.sort(np.concatenate([heavy[:40], np.arange(0, idx.n_rows, 37)]))
+    q = _gather_rows(idx, np.unique(rows))
+    monkeypatch.setenv("SD_HYBRID", "2")
+    assert _lib.device_index(sd.to_device(_host(idx), dtype)).heavy_rows == len(heavy)
+    for name in DOT_FAMILY:
+        a, b = (q, idx) if name not in ("dice", "jaccard", "russelrao") else (q.with_values(np.ones(q.nnz)),
+                                                                              idx.with_values(np.ones(idx.nnz)))
+        a, b = _host(a), _host(b)
+        spec = sd.metric_registry(name)
+        got = sd.pairwise_distances(a, b, spec, dtype=dtype)
+        ref = O.pairwise_distances(a, b, name)
+        assert_parity(got, ref, a, b, name, dtype, what=f"hybrid/{name}")
+        monkeypatch.setenv("SD_HYBRID", "0")
+        sweep = sd.pairwise_distances(_host(a), _host(b), spec, dtype=dtype)
+        monkeypatch.setenv("SD_HYBRID", "2")
+        assert_parity(got, sweep, a, b, name, dtype, what=f"hybrid vs sweep/{name}")
+    torch.cuda.synchronize()
