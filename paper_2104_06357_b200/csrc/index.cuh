@@ -26,6 +26,9 @@ struct sd_index {
   uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
   void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
   int64_t bytes = 0;
+  // cosine: a copy of `post` with every value divided by its row's L2 norm,
+  // built on the first cosine call (the epilogue then needs no index-row statistic)
+  void* post_cos = nullptr;
   // probability that two random postings of one tile belong to the same row
   // (sum over tiles of sum d_j^2 / sum over tiles of (sum d_j)^2): why packing
   // several columns into one warp step does not pay on power-law indexes

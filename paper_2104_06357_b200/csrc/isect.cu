@@ -162,6 +162,46 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
   return SD_OK;
 }
 
+// post_cos[p] = post[p] with the value times 1/||b_row|| (the tile of a
+// posting follows from its (tile, column) key range)
+template <typename T>
+__global__ void post_scale_kernel(const uint32_t* __restrict__ colptr, const Posting<T>* __restrict__ post,
+                                  int64_t n_keys, int64_t n_cols, int tile, const T* __restrict__ inv,
+                                  Posting<T>* __restrict__ out) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n_keys; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t base = (k / n_cols) * tile;
+    for (uint32_t p = colptr[k]; p < colptr[k + 1]; ++p) {
+      Posting<T> q = post[p];
+      q.v = mul_rn(q.v, inv[base + q.j]);
+      out[p] = q;
+    }
+  }
+}
+
+static int ensure_post_cos(sd_index* ix, const void* inv, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(ix->mu);
+  if (ix->post_cos) return SD_OK;
+  const size_t ps = ix->dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>);
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, ps * std::max<int64_t>(1, ix->nnz)) != cudaSuccess) {
+    set_error("cudaMalloc failed for the scaled cosine postings");
+    return SD_E_CUDA;
+  }
+  const int64_t n_keys = ix->n_tiles * ix->n_cols;
+  const int blocks = int(std::min<int64_t>((n_keys + 255) / 256, int64_t(num_sms()) * 16));
+  const int rc = SD_DISPATCH_DTYPE(ix->dtype, T, [&]() -> int {
+    post_scale_kernel<T><<<std::max(1, blocks), 256, 0, st>>>(ix->colptr, static_cast<const Posting<T>*>(ix->post),
+                                                              n_keys, ix->n_cols, ix->tile, static_cast<const T*>(inv),
+                                                              static_cast<Posting<T>*>(buf));
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  });
+  if (rc != SD_OK) { cudaFree(buf); return rc; }
+  ix->post_cos = buf;
+  ix->bytes += int64_t(ps) * ix->nnz;
+  return SD_OK;
+}
+
 // Work plan (one CTA, no library sort): queries ordered by descending
 // floor(log2(degree)) (LPT), each split into items of `tpi` consecutive tiles
 // so that every item costs about total/(8·warps) — a power-law query of
@@ -317,8 +357,11 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   const int64_t band = band0;
   // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
   // computed densely; the sweep skips them
+  // cosine over postings pre-divided by the index-row norms (built once per index)
+  const bool cos_scaled = md->metric == SD_M_COSINE && sb.s[1] != nullptr && getenv("SD_COS_RAW") == nullptr;
+  if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
   HybridState hs;
-  if (topk == 0 && ck == C_MUL && !tile_major && ix->n_heavy > 0 && hybrid_enabled() &&
+  if (topk == 0 && ck == C_MUL && ix->n_heavy > 0 && hybrid_enabled() &&
       (ix->n_tiles >= 4 || hybrid_forced()))  // small indexes: the sweep is cheap, keep it exact
     SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
   plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
@@ -342,6 +385,9 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.item_off = item_off.as<int64_t>(); args.item_pos = item_pos.as<int32_t>();
     args.counter = counter.as<unsigned int>();
     args.tile_major = tile_major;
+    args.skip = hs.nhq > 0 ? hs.qid.as<int32_t>() : nullptr;
+    args.cos_scaled = cos_scaled ? 1 : 0;
+    if (cos_scaled) args.post = static_cast<const Posting<T>*>(ix->post_cos);
     const char* de = getenv("SD_ISECT_DEBUG");
     args.debug = de ? atoi(de) : 0;
     args.band = band;
@@ -372,6 +418,7 @@ int sd_index_free(sd_index* ix) {
   if (ix->post) cudaFree(ix->post);
   if (ix->post_rank) cudaFree(ix->post_rank);
   if (ix->topb) cudaFree(ix->topb);
+  if (ix->post_cos) cudaFree(ix->post_cos);
   for (auto& e : ix->stat_cache) cudaFree(e.buf);
   sd::hybrid_index_free(ix);
   delete ix;

@@ -34,6 +34,8 @@ struct IsectArgs {
   const int32_t* item_pos;  // item -> plan position
   unsigned int* counter;
   int tile_major;           // items are (tile, position) pairs in tile-major order
+  int cos_scaled;           // cosine: postings hold b_jc / ||b_j|| (sd_index post_cos)
+  const int32_t* skip;      // rows with skip[i] >= 0 belong to the hybrid path (tile-major plan)
   int debug;                // timing experiments (SD_ISECT_DEBUG): 1 skip the sweep, 2 skip the epilogue
   int64_t band;             // tiles per band (band-major plan)
   int strict;
@@ -203,7 +205,8 @@ template <typename T, int M>
 __device__ __forceinline__ T isect_cell(const IsectArgs<T>& a, T gv, T gcv, T ra0, T ra1, T gb0, T gb1,
                                         bool fast_zero, T zero_val, uint32_t& f) {
   if constexpr (M == SD_M_COSINE) {
-    if (ra0 > T(0)) return sub_rn(T(1), mul_rn(gv, mul_rn(ra1, gb1)));  // gb1 = 1/||b|| (0 if empty)
+    if (ra0 > T(0))  // gb1 = 1/||b|| (0 if empty); scaled postings already carry it
+      return a.cos_scaled ? sub_rn(T(1), mul_rn(gv, ra1)) : sub_rn(T(1), mul_rn(gv, mul_rn(ra1, gb1)));
     return gb0 == T(0) ? T(0) : T(1);  // empty query row (metrics.py:116-118): 0 against empty rows, else 1
   } else {
     if (fast_zero && gv == T(0)) return zero_val;
@@ -302,6 +305,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
       t1 = tmin<int64_t>(tmin<int64_t>(a.n_tiles, (band + 1) * a.band), t0 + tpi);
     }
     const int64_t i = a.order[pos];
+    if (a.skip && a.skip[i] >= 0) continue;
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
     const T ra0 = a.sa0 ? a.sa0[i] : T(0);
     const T ra1 = a.sa1 ? a.sa1[i] : T(0);
@@ -424,8 +428,11 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         // pointers advanced per group, no bounds tests, and the per-query
         // cosine branch hoisted out of the cell loop
         if (vec_out && nt == TJ && TJ % (EPF * 128) == 0) {
+          // nz: 0 generic cell, 1 cosine of a non-empty query, 2 the same over
+          // scaled postings (no per-cell index statistic at all)
           auto run = [&](auto nz) {
-            constexpr bool NZ = decltype(nz)::value;
+            constexpr int NZM = decltype(nz)::value;
+            constexpr bool NZ = NZM > 0;
             T* op = a.out + i * a.ldo + j0 + 4 * lane;
             const T* p0 = SB0 ? a.sb0 + j0 + 4 * lane : nullptr;
             const T* p1 = SB1 ? a.sb1 + j0 + 4 * lane : nullptr;
@@ -439,13 +446,15 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               sts4_zero(sa + off * ES, T(0));
               if constexpr (KL) { lds4(sc + off * ES, c); sts4_zero(sc + off * ES, T(0)); }
               if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) V4<T>::load(p0 + off, b0);
-              if constexpr (SB1) V4<T>::load(p1 + off, b1);
+              if constexpr (SB1 && NZM != 2) V4<T>::load(p1 + off, b1);
             };
             auto finish = [&](uint32_t off, const T* v, const T* c, const T* b0, const T* b1) {
               T r[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                if constexpr (M == SD_M_COSINE && NZ) {
+                if constexpr (M == SD_M_COSINE && NZM == 2) {
+                  r[u] = sub_rn(T(1), mul_rn(v[u], ra1));
+                } else if constexpr (M == SD_M_COSINE && NZ) {
                   r[u] = sub_rn(T(1), mul_rn(v[u], mul_rn(ra1, b1[u])));
                 } else {
                   uint32_t f = 0;
@@ -468,8 +477,9 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               }
             }
           };
-          if (M == SD_M_COSINE && ra0 > T(0)) run(std::true_type{});
-          else run(std::false_type{});
+          if (M == SD_M_COSINE && ra0 > T(0) && a.cos_scaled) run(std::integral_constant<int, 2>{});
+          else if (M == SD_M_COSINE && ra0 > T(0)) run(std::integral_constant<int, 1>{});
+          else run(std::integral_constant<int, 0>{});
           __syncwarp();
           continue;
         }
@@ -675,7 +685,9 @@ int launch_heavy_rows(IsectArgs<T>& a, const int32_t* hq, int nhq, const int32_t
     SD_TRY(prepare_smem(heavy_rows_kernel<T, M>, smem, "heavy_rows_kernel"));
     const int64_t nblk = (a.n + JB - 1) / JB;
     const int blocks = int(tmin<int64_t>(nblk, int64_t(num_sms()) * 8));
-    heavy_rows_kernel<T, M><<<blocks, 256, smem, st>>>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, JB);
+    IsectArgs<T> raw = a;
+    raw.cos_scaled = 0;  // the dense path sums raw products
+    heavy_rows_kernel<T, M><<<blocks, 256, smem, st>>>(raw, hq, nhq, hid, dqh, hpad, dlh, qpad, JB);
     SD_LAUNCH_CHECK();
     return SD_OK;
   }
