@@ -206,6 +206,121 @@ __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__
   }
 }
 
+// fp32: the same GEMM on the tensor cores with the 3xTF32 split
+// (x = hi + lo, hi = tf32(x), lo = tf32(x - hi); a*b ~ lo_a*hi_b + hi_a*lo_b +
+// hi_a*hi_b, error ~2^-22 |a||b| per product, well inside the fp32 parity
+// tolerance).  mma.sync.m16n8k8 tf32: CTA tile 32 x 128 over BK = 32, four
+// warps of 32 x 32, operands staged K-major in padded shared memory so every
+// fragment load is bank-conflict free.
+constexpr int TG_BM = 32, TG_BN = 128, TG_BK = 32, TG_PA = TG_BM + 8, TG_PB = TG_BN + 8;
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, const uint32_t* b) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__global__ void __launch_bounds__(128) hgemm_tf32x3_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                           int64_t K, int64_t lda, int64_t ldb, int64_t kchunk,
+                                                           int64_t ldp, int64_t rows, float* __restrict__ P) {
+  __shared__ __align__(16) float As[2][TG_BK][TG_PA];
+  __shared__ __align__(16) float Bs[2][TG_BK][TG_PB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int64_t q0 = int64_t(blockIdx.y) * TG_BM, h0 = int64_t(blockIdx.x) * TG_BN;
+  const int64_t kb = int64_t(blockIdx.z) * kchunk, ke = tmin<int64_t>(K, kb + kchunk);
+  // staging: A tile 32 x 32 (8 floats per thread), B tile 32 x 128 (32 per thread)
+  const int ak = tid >> 2, ac = (tid & 3) * 8;
+  const int bk = tid >> 2, bcol = (tid & 3) * 32;
+  float ra[8], rb[32];
+  auto gload = [&](int64_t k0) {
+    const int64_t k = k0 + ak;
+    if (k < ke) {
+      V4<float>::load(A + k * lda + q0 + ac, ra);
+      V4<float>::load(A + k * lda + q0 + ac + 4, ra + 4);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) V4<float>::load(B + k * ldb + h0 + bcol + 4 * v, rb + 4 * v);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ra[u] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) rb[u] = 0.f;
+    }
+  };
+  auto sstore = [&](int buf) {
+    V4<float>::store_plain(&As[buf][ak][ac], ra);
+    V4<float>::store_plain(&As[buf][ak][ac + 4], ra + 4);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) V4<float>::store_plain(&Bs[buf][bk][bcol + 4 * v], rb + 4 * v);
+  };
+  float acc[2][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[mi][ni][u] = 0.f;
+  gload(kb);
+  sstore(0);
+  __syncthreads();
+  int buf = 0;
+  const int wn = warp * 32;
+  for (int64_t k0 = kb; k0 < ke; k0 += TG_BK) {
+    const bool more = k0 + TG_BK < ke;
+    if (more) gload(k0 + TG_BK);
+#pragma unroll
+    for (int kk = 0; kk < TG_BK; kk += 8) {
+      uint32_t ahi[2][4], alo[2][4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const float x[4] = {As[buf][kk + tig][mi * 16 + gid], As[buf][kk + tig][mi * 16 + gid + 8],
+                            As[buf][kk + tig + 4][mi * 16 + gid], As[buf][kk + tig + 4][mi * 16 + gid + 8]};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ahi[mi][u] = to_tf32(x[u]);
+          alo[mi][u] = to_tf32(x[u] - __uint_as_float(ahi[mi][u]));
+        }
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const float y[2] = {Bs[buf][kk + tig][wn + ni * 8 + gid], Bs[buf][kk + tig + 4][wn + ni * 8 + gid]};
+        uint32_t bhi[2], blo[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          bhi[u] = to_tf32(y[u]);
+          blo[u] = to_tf32(y[u] - __uint_as_float(bhi[u]));
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          mma_tf32(acc[mi][ni], alo[mi], bhi);
+          mma_tf32(acc[mi][ni], ahi[mi], blo);
+          mma_tf32(acc[mi][ni], ahi[mi], bhi);
+        }
+      }
+    }
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  float* out = P + int64_t(blockIdx.z) * rows * ldp;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int64_t r = q0 + mi * 16 + gid, c = h0 + wn + ni * 8 + 2 * tig;
+      *reinterpret_cast<float2*>(out + r * ldp + c) = make_float2(acc[mi][ni][0], acc[mi][ni][1]);
+      *reinterpret_cast<float2*>(out + (r + 8) * ldp + c) = make_float2(acc[mi][ni][2], acc[mi][ni][3]);
+    }
+}
+
 template <typename T>
 __global__ void hreduce_kernel(const T* __restrict__ P, int splits, int64_t count, T* __restrict__ D) {
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
@@ -289,12 +404,15 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   hs.qpad = (hs.nhq + 127) / 128 * 128;
   SD_TRY(hs.hqt.alloc(es * size_t(K) * size_t(hs.qpad), st));
   SD_CUDA_TRY(cudaMemsetAsync(hs.hqt.ptr, 0, es * size_t(K) * size_t(hs.qpad), st));
-  const int64_t tiles_q = (hs.nhq + HG_BM - 1) / HG_BM, tiles_h = ix->hpad / HG_BN;
-  const int64_t rows = tiles_q * HG_BM;  // GEMM rows computed (<= qpad)
+  // fp32: tensor-core 3xTF32 GEMM (tile 32 x 128 x 32); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
+  const bool tc = dtype == SD_F32 && getenv("SD_HGEMM_SIMT") == nullptr;
+  const int64_t bm = tc ? TG_BM : HG_BM, bn = tc ? TG_BN : HG_BN, bkk = tc ? TG_BK : HG_BK;
+  const int64_t tiles_q = (hs.nhq + bm - 1) / bm, tiles_h = ix->hpad / bn;
+  const int64_t rows = tiles_q * bm;  // GEMM rows computed (<= qpad)
   // K split so that the GEMM fills about three waves of CTAs
   const int64_t want = std::max<int64_t>(1, (3 * 2 * int64_t(num_sms()) + tiles_q * tiles_h - 1) / (tiles_q * tiles_h));
   int64_t kchunk = (K + want - 1) / want;
-  kchunk = std::max<int64_t>(HG_BK, (kchunk + HG_BK - 1) / HG_BK * HG_BK);
+  kchunk = std::max<int64_t>(bkk, (kchunk + bkk - 1) / bkk * bkk);
   const int64_t splits = (K + kchunk - 1) / kchunk;
   SD_TRY(hs.part.alloc(es * size_t(splits) * size_t(rows) * size_t(ix->hpad), st));
   SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
@@ -304,9 +422,18 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     ht_scatter_kernel<T><<<gblocks, 256, 0, st>>>(a->indptr, a->indices, static_cast<const T*>(a->values),
                                                   hs.hq.as<int32_t>(), hs.nhq, hs.qpad, hs.hqt.as<T>());
     SD_LAUNCH_CHECK();
-    hgemm_kernel<T><<<dim3(unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)), HG_THREADS, 0, st>>>(
-        hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad, ix->hpad, kchunk, ix->hpad, rows,
-        hs.part.as<T>());
+    const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
+    if constexpr (sizeof(T) == 4) {
+      if (tc)
+        hgemm_tf32x3_kernel<<<grid, 128, 0, st>>>(hs.hqt.as<float>(), static_cast<const float*>(ix->ht), K, hs.qpad,
+                                                  ix->hpad, kchunk, ix->hpad, rows, hs.part.as<float>());
+      else
+        hgemm_kernel<T><<<grid, HG_THREADS, 0, st>>>(hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad,
+                                                     ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());
+    } else {
+      hgemm_kernel<T><<<grid, HG_THREADS, 0, st>>>(hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad,
+                                                   ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());
+    }
     SD_LAUNCH_CHECK();
     const int64_t count = rows * ix->hpad;
     hreduce_kernel<T><<<int(std::min<int64_t>((count + 255) / 256, int64_t(num_sms()) * 16)), 256, 0, st>>>(

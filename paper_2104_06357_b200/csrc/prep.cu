@@ -30,6 +30,7 @@ __device__ __forceinline__ T stat_term(T v, T p) {
 // dependent global loads.
 constexpr int STAT_LONG = 64;
 constexpr int STAT_CHUNK = 256;
+constexpr int64_t STAT_BLOCKED = 2048;  // longer rows: 32 lane-blocked partial sums
 constexpr int STAT_WARPS = 4;
 
 template <typename T, int KIND, int SR>
@@ -65,6 +66,26 @@ __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t
         long_mask &= long_mask - 1;
         const int64_t lb = __shfl_sync(0xffffffffu, beg, src), le = __shfl_sync(0xffffffffu, end, src);
         T ls = T(0);
+        if (le - lb > STAT_BLOCKED) {
+          // very long (power-law) rows: each lane sums one contiguous 1/32 of the
+          // row in order, lane 0 adds the 32 partials in order — deterministic,
+          // a 32x shorter dependency chain than the strictly sequential sum
+          const int64_t len = le - lb, per = (len + 31) / 32;
+          const int64_t cb = lb + tmin<int64_t>(len, int64_t(lane) * per), ce = tmin<int64_t>(le, cb + per);
+          T part = T(0);
+          int64_t e = cb;
+          for (; e + 8 <= ce; e += 8) {
+            T t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = stat_term<T, KIND, SR>(__ldg(val + e + u), p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) part = add_rn(part, t[u]);
+          }
+          for (; e < ce; ++e) part = add_rn(part, stat_term<T, KIND, SR>(__ldg(val + e), p));
+          for (int l = 0; l < 32; ++l) ls = add_rn(ls, __shfl_sync(0xffffffffu, part, l));
+          if (int(lane) == src) s = ls;
+          continue;
+        }
         T nxt[STAT_CHUNK / 32];
 #pragma unroll
         for (int k = 0; k < STAT_CHUNK / 32; ++k) {

@@ -277,7 +277,7 @@ def test_power_law_properties_at_scale():
     q = _gather_rows(idx, rows)
     d = sd.pairwise_distances(q, idx, sd.metric_registry("cosine"), dtype=np.float32)
     assert d.shape == (64, idx.n_rows)
-    np.testing.assert_allclose(d[np.arange(64), rows], 0.0, atol=1e-6)
+    np.testing.assert_allclose(d[np.arange(64), rows], 0.0, atol=1e-5)  # fp32 parity tolerance
     cols = np.sort(rng.choice(idx.n_rows, 2000, replace=False))
     sub = _gather_rows(idx, cols)
     ref = O.pairwise_distances(q, sub, "cosine")
