@@ -340,7 +340,11 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // from HBM about once while every query sweeps the resident band; bands are
   // split evenly (no short tail band).  SD_ISECT_BAND overrides (tuning).
   const char* be0 = getenv("SD_ISECT_BAND");
-  const int64_t post_bytes = std::max<int64_t>(1, ix->bytes);
+  // bytes the sweep streams: postings + their (tile, column) ranges (not the
+  // hybrid block or the other metric's posting copy, which it never touches)
+  const int64_t post_bytes = std::max<int64_t>(
+      1, ix->nnz * int64_t(dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>)) +
+             int64_t(sizeof(uint32_t)) * (ix->n_tiles * ix->n_cols + 1));
   const int64_t n_bands0 = (post_bytes + l2_bytes() - 1) / l2_bytes();
   const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
   const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : auto_band));
