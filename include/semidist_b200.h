@@ -191,8 +191,10 @@ SD_API int64_t sd_index_heavy_rows(const sd_index* index);
  * floats) receives device times of the phases {norms, pass1, pass2,
  * expansion} of metrics.py:325-374 measured with CUDA events; passing it
  * synchronises `stream`.  On the fused path "pass1" is the intersection
- * kernel and "pass2" the one-sided NAMM sums that replace the complement
- * sweep. */
+ * kernel alone, "pass2" the one-sided NAMM sums that replace the complement
+ * sweep or, for dot-family metrics, the dense path of the
+ * heavy query rows (GEMM + gather, hybrid.cu), and "expansion" the epilogue
+ * of those heavy rows. */
 SD_API int sd_pairwise(const sd_csr* a, const sd_csr* b, const sd_index* index, int dtype,
                 const sd_metric_desc* metric, const sd_strategy* strategy,
                 void* out, int64_t ldo, uint32_t* dev_flags, sd_report* report,

@@ -81,32 +81,7 @@ static int transformed(const sd_csr* in, int dtype, const sd_metric_desc* md, sd
 }
 
 // Device time of the phases {norms, pass1, pass2, expansion} (metrics.py:325-374).
-struct PhaseTimer {
-  float* out;
-  cudaStream_t st;
-  cudaEvent_t ev[8] = {};
-  bool used[4] = {false, false, false, false};
-  PhaseTimer(float* o, cudaStream_t s) : out(o), st(s) {
-    if (out)
-      for (auto& e : ev) cudaEventCreate(&e);
-  }
-  ~PhaseTimer() {
-    if (out)
-      for (auto& e : ev) cudaEventDestroy(e);
-  }
-  void begin(int ph) { if (out) { cudaEventRecord(ev[2 * ph], st); used[ph] = true; } }
-  void end(int ph) { if (out) cudaEventRecord(ev[2 * ph + 1], st); }
-  int finish() {
-    if (!out) return SD_OK;
-    SD_CUDA_TRY(cudaStreamSynchronize(st));
-    for (int ph = 0; ph < 4; ++ph) {
-      out[ph] = 0.f;
-      if (used[ph]) SD_CUDA_TRY(cudaEventElapsedTime(&out[ph], ev[2 * ph], ev[2 * ph + 1]));
-    }
-    return SD_OK;
-  }
-};
-enum { PH_NORMS = 0, PH_PASS1 = 1, PH_PASS2 = 2, PH_EXPANSION = 3 };
+
 
 // The two-pass engine route of pairwise_distances_detail (metrics.py:340-375).
 static int engine_pairwise(const sd_csr* a, const sd_csr* b, int dtype, const sd_metric_desc* md,
@@ -171,9 +146,7 @@ static int fused_run(const sd_csr* a, const sd_csr* b, const sd_index* index, in
   int rc = isect_stats(a, b, ix, dtype, md, sabuf, sbbuf, &sa, &sb, st);
   tm.end(ph_stats);
   if (rc == SD_OK) {
-    tm.begin(PH_PASS1);
-    rc = isect_run(a, b, ix, dtype, md, sa, sb, out, ldo, topk, base, out_d, out_i, flags, st);
-    tm.end(PH_PASS1);
+    rc = isect_run(a, b, ix, dtype, md, sa, sb, out, ldo, topk, base, out_d, out_i, flags, &tm, st);
   }
   if (own) {
     cudaStreamSynchronize(st);

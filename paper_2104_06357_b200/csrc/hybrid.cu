@@ -330,6 +330,12 @@ __global__ void hreduce_kernel(const T* __restrict__ P, int splits, int64_t coun
   }
 }
 
+// dense rows in flight per lane in the gather
+#ifndef SD_HGATHER_UNROLL
+#define SD_HGATHER_UNROLL 8
+#endif
+constexpr int HGU = SD_HGATHER_UNROLL;
+
 // DLH[j][q] = sum_c b_jc * HQT[c][q] over light index rows j (heavy rows are
 // the GEMM's); one warp per (row, 128-wide block of heavy queries), ascending
 // column order, 8 dense rows in flight per lane.  Rows are taken from a
@@ -339,7 +345,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                       const T* __restrict__ val, const int32_t* __restrict__ lrows,
                                                       int64_t n_light, const T* __restrict__ D, int64_t ld,
-                                                      int64_t nblk, unsigned long long* counter, T* __restrict__ out) {
+                                                      int64_t nblk, int64_t width, unsigned long long* counter,
+                                                      T* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = (unsigned long long)(n_light * nblk);
   while (true) {
@@ -350,24 +357,27 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
     const int64_t j = lrows[it / nblk], blk = int64_t(it % nblk);
     const int64_t beg = ptr[j], end = ptr[j + 1];
     const T* dcol = D + blk * 128 + 4 * lane;
+    // lanes past the last heavy query of the block load nothing (no L2 sectors)
+    const bool lane_on = blk * 128 + 4 * lane < width;
     T acc[4] = {T(0), T(0), T(0), T(0)};
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
       const bool ok = e0 + lane < end;
       const int32_t cl = ok ? idx[e0 + lane] : 0;
       const T vl = ok ? val[e0 + lane] : T(0);
       const int nn = int(tmin<int64_t>(32, end - e0));
-      for (int u0 = 0; u0 < nn; u0 += 8) {
-        T d[8][4];
-        T x[8];
+      for (int u0 = 0; u0 < nn; u0 += HGU) {
+        T d[HGU][4];
+        T x[HGU];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < HGU; ++u) {
           const int src = (u0 + u) & 31;
           const int32_t c = __shfl_sync(0xffffffffu, cl, src);
           x[u] = __shfl_sync(0xffffffffu, vl, src);
-          if (u0 + u < nn) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
+          if (u0 + u < nn && lane_on) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
+          else d[u][0] = d[u][1] = d[u][2] = d[u][3] = T(0);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < HGU; ++u)
           if (u0 + u < nn)
 #pragma unroll
             for (int k = 0; k < 4; ++k) acc[k] = fma_rn(x[u], d[u][k], acc[k]);
@@ -444,7 +454,7 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T>, 256, 0));
     hgather_kernel<T><<<std::max(1, per_sm) * num_sms(), 256, 0, st>>>(
         b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hs.qpad,
-        nblk, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+        nblk, int64_t(hs.nhq), hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
     SD_LAUNCH_CHECK();
     return SD_OK;
   });

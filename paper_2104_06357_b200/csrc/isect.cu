@@ -321,7 +321,7 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtyp
 // Fused pairwise distances / kNN over the intersection path.
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
-              void* out_d, int64_t* out_i, uint32_t* flags, cudaStream_t st) {
+              void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, cudaStream_t st) {
   const int ck = metric_contrib(md->metric);
   if (ck < 0) { set_error("metric not decomposable over intersections"); return SD_E_UNSUPPORTED; }
   if (ix->dtype != dtype || ix->n_rows != b->n_rows || ix->n_cols != b->n_cols) {
@@ -366,8 +366,11 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
   HybridState hs;
   if (topk == 0 && ck == C_MUL && ix->n_heavy > 0 && hybrid_enabled() &&
-      (ix->n_tiles >= 4 || hybrid_forced()))  // small indexes: the sweep is cheap, keep it exact
+      (ix->n_tiles >= 4 || hybrid_forced())) {  // small indexes: the sweep is cheap, keep it exact
+    if (tm) tm->begin(PH_PASS2);
     SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
+    if (tm) tm->end(PH_PASS2);
+  }
   plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
                                   hs.nhq > 0 ? hs.qid.as<int32_t>() : nullptr,
                                   order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
@@ -405,10 +408,15 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.topa = static_cast<const T*>(sa.s[0]);
     args.topb = static_cast<const T*>(ix->topb);
     args.b_ptr = b->indptr; args.b_idx = b->indices; args.b_val = static_cast<const T*>(b->values);
+    if (tm) tm->begin(PH_PASS1);
     SD_TRY(isect_launch(args, md->metric, W, st));
-    if (hs.nhq > 0)
+    if (tm) tm->end(PH_PASS1);
+    if (hs.nhq > 0) {
+      if (tm) tm->begin(PH_EXPANSION);
       SD_TRY(isect_heavy_rows(args, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(), ix->hpad,
                               hs.dlh.as<T>(), hs.qpad, st));
+      if (tm) tm->end(PH_EXPANSION);
+    }
     if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
     return SD_OK;
   });

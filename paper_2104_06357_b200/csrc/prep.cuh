@@ -46,6 +46,35 @@ int expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd_me
            int64_t n_cols, const Stats& sa, const Stats& sb, const void* miss,
            uint32_t* flags, cudaStream_t st);
 
+// Device times of the phases of one call (sd_pairwise's phase_ms): events on
+// the call's stream, read once at the end.
+struct PhaseTimer {
+  float* out;
+  cudaStream_t st;
+  cudaEvent_t ev[8] = {};
+  bool used[4] = {false, false, false, false};
+  PhaseTimer(float* o, cudaStream_t s) : out(o), st(s) {
+    if (out)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  ~PhaseTimer() {
+    if (out)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void begin(int ph) { if (out) { cudaEventRecord(ev[2 * ph], st); used[ph] = true; } }
+  void end(int ph) { if (out) cudaEventRecord(ev[2 * ph + 1], st); }
+  int finish() {
+    if (!out) return SD_OK;
+    SD_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int ph = 0; ph < 4; ++ph) {
+      out[ph] = 0.f;
+      if (used[ph]) SD_CUDA_TRY(cudaEventElapsedTime(&out[ph], ev[2 * ph], ev[2 * ph + 1]));
+    }
+    return SD_OK;
+  }
+};
+enum { PH_NORMS = 0, PH_PASS1 = 1, PH_PASS2 = 2, PH_EXPANSION = 3 };
+
 int metric_semiring(int metric);
 int default_tile(int dtype);
 int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream_t st);
@@ -53,7 +82,7 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype,
                 Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st);
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
-              void* out_d, int64_t* out_i, uint32_t* flags, cudaStream_t st);
+              void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, cudaStream_t st);
 int topk_rows(const void* dist, int64_t m, int64_t n, int64_t ldd, int dtype, int k, int64_t base,
               void* od, int64_t* oi, cudaStream_t st);
 int topk_merge(const void* cd, const int64_t* ci, int64_t m, int lists, int k, int dtype, void* od,
