@@ -356,7 +356,7 @@ def run_ours(args):
         # query rows the dense heavy-row path serves instead of the sweep
         # (hybrid.cu: dot-family metrics, index with a heavy-row block, >= 4 tiles)
         deg = np.diff(np.asarray(queries.indptr))
-        theta = max(64, (index.n_cols + 15) // 16)
+        theta = max(64, (index.n_cols + 31) // 32)
         n_tiles = -(-n // ix.tile_rows)
         heavy_q = (min(1024, int((deg >= theta).sum())) if ix.heavy_rows > 0 and n_tiles >= 4
                    and head in ("cosine", "euclidean", "correlation", "dot", "dice", "jaccard", "hellinger",

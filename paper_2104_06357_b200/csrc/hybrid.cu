@@ -1,7 +1,7 @@
 // hybrid.cu — dense path for heavy query rows (dot-family metrics).
 //
 // On power-law data a few query rows carry most of the query nonzeros (C2:
-// the 0.8% of queries with >= n_cols/16 nonzeros hold 74% of them) and a few
+// the 1.4% of queries with >= n_cols/32 nonzeros hold ~80% of them) and a few
 // index rows most of the index nonzeros.  In the intersection sweep a query
 // costs one warp step per (query column, index tile) pair, so those heavy
 // queries dominate the sweep although they are a handful of output rows.
@@ -18,6 +18,7 @@
 // sparse intersection sums up to rounding (products with an absent entry are
 // exact zeros).
 #include <algorithm>
+#include <string>
 #include <cstdlib>
 #include <vector>
 #include "index.cuh"
@@ -36,7 +37,7 @@ int64_t env_i64(const char* name, int64_t dflt) {
 }  // namespace
 
 int64_t hybrid_threshold(int64_t n_cols) {
-  return std::max<int64_t>(64, env_i64("SD_HEAVY_DEG", (n_cols + 15) / 16));
+  return std::max<int64_t>(64, env_i64("SD_HEAVY_DEG", (n_cols + 31) / 32));
 }
 
 // SD_HYBRID: 0 off, 1 automatic (default), 2 forced even for small indexes (tests)
@@ -96,6 +97,17 @@ int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st
     SD_LAUNCH_CHECK();
     return SD_OK;
   }));
+  if (dtype == SD_F32) {  // A operand image of the tensor-core GEMM
+    const int64_t nks = (b->n_cols + tc_kstep() - 1) / tc_kstep();
+    const int64_t tbytes = (pad / 128) * nks * 2 * 128 * tc_kstep() * 4;
+    if (cudaMalloc(&ix->ht_tiled, tbytes) != cudaSuccess) {
+      set_error("cudaMalloc failed for the hybrid index (tiled)");
+      return SD_E_CUDA;
+    }
+    SD_TRY(tiled_operand(b, drows.as<int32_t>(), nh, 128, nks, ix->ht_tiled, st));
+    ix->nks = nks;
+    ix->bytes += tbytes;
+  }
   SD_CUDA_TRY(cudaStreamSynchronize(st));  // the host copies above must outlive the transfers
   ix->heavy_deg = theta;
   ix->n_heavy = nh;
@@ -109,6 +121,8 @@ void hybrid_index_free(sd_index* ix) {
   if (ix->hid) cudaFree(ix->hid);
   if (ix->ht) cudaFree(ix->ht);
   if (ix->lrows) cudaFree(ix->lrows);
+  if (ix->ht_tiled) cudaFree(ix->ht_tiled);
+  ix->ht_tiled = nullptr;
   ix->hid = nullptr;
   ix->ht = nullptr;
   ix->lrows = nullptr;
@@ -357,8 +371,6 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
     const int64_t j = lrows[it / nblk], blk = int64_t(it % nblk);
     const int64_t beg = ptr[j], end = ptr[j + 1];
     const T* dcol = D + blk * 128 + 4 * lane;
-    // lanes past the last heavy query of the block load nothing (no L2 sectors)
-    const bool lane_on = blk * 128 + 4 * lane < width;
     T acc[4] = {T(0), T(0), T(0), T(0)};
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
       const bool ok = e0 + lane < end;
@@ -373,8 +385,7 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
           const int src = (u0 + u) & 31;
           const int32_t c = __shfl_sync(0xffffffffu, cl, src);
           x[u] = __shfl_sync(0xffffffffu, vl, src);
-          if (u0 + u < nn && lane_on) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
-          else d[u][0] = d[u][1] = d[u][2] = d[u][3] = T(0);
+          if (u0 + u < nn) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
         }
 #pragma unroll
         for (int u = 0; u < HGU; ++u)
@@ -414,16 +425,27 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   hs.qpad = (hs.nhq + 127) / 128 * 128;
   SD_TRY(hs.hqt.alloc(es * size_t(K) * size_t(hs.qpad), st));
   SD_CUDA_TRY(cudaMemsetAsync(hs.hqt.ptr, 0, es * size_t(K) * size_t(hs.qpad), st));
-  // fp32: tensor-core 3xTF32 GEMM (tile 32 x 128 x 32); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
-  const bool tc = dtype == SD_F32 && getenv("SD_HGEMM_SIMT") == nullptr;
-  const int64_t bm = tc ? TG_BM : HG_BM, bn = tc ? TG_BN : HG_BN, bkk = tc ? TG_BK : HG_BK;
+  // fp32: tcgen05 3xTF32 GEMM (M = 128 heavy index rows x N = all heavy
+  // queries, hgemm_tc.cu) when they fit one tile (<= 256), else mma.sync
+  // 3xTF32 (tile 32 x 128 x 32); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
+  const char* ge = getenv("SD_HGEMM");  // experiment override: "simt", "mma"
+  const bool simt = ge && std::string(ge) == "simt";
+  const bool tc5 = dtype == SD_F32 && ix->ht_tiled && hs.nhq <= 256 && !simt && !(ge && std::string(ge) == "mma");
+  const bool tc = dtype == SD_F32 && !simt && !tc5;
+  const int64_t bm = tc5 ? (hs.nhq + 15) / 16 * 16 : tc ? TG_BM : HG_BM;
+  const int64_t bn = tc5 ? 128 : tc ? TG_BN : HG_BN, bkk = tc5 ? tc_kstep() : tc ? TG_BK : HG_BK;
   const int64_t tiles_q = (hs.nhq + bm - 1) / bm, tiles_h = ix->hpad / bn;
   const int64_t rows = tiles_q * bm;  // GEMM rows computed (<= qpad)
-  // K split so that the GEMM fills about three waves of CTAs
-  const int64_t want = std::max<int64_t>(1, (3 * 2 * int64_t(num_sms()) + tiles_q * tiles_h - 1) / (tiles_q * tiles_h));
+  // K split so that the GEMM fills about two (tensor-core) or six waves of CTAs
+  const int64_t waves = tc5 ? 2 : 3 * 2;
+  const int64_t want = std::max<int64_t>(1, (waves * int64_t(num_sms()) + tiles_q * tiles_h - 1) / (tiles_q * tiles_h));
   int64_t kchunk = (K + want - 1) / want;
   kchunk = std::max<int64_t>(bkk, (kchunk + bkk - 1) / bkk * bkk);
   const int64_t splits = (K + kchunk - 1) / kchunk;
+  if (tc5) {  // B operand image of this call's heavy queries
+    SD_TRY(hs.hq_tiled.alloc(size_t(ix->nks) * 2 * size_t(bm) * tc_kstep() * 4, st));
+    SD_TRY(tiled_operand(a, hs.hq.as<int32_t>(), hs.nhq, int(bm), ix->nks, hs.hq_tiled.ptr, st));
+  }
   SD_TRY(hs.part.alloc(es * size_t(splits) * size_t(rows) * size_t(ix->hpad), st));
   SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
   SD_TRY(hs.dlh.alloc(es * size_t(std::max<int64_t>(1, b->n_rows)) * size_t(hs.qpad), st));
@@ -434,7 +456,10 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     SD_LAUNCH_CHECK();
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
     if constexpr (sizeof(T) == 4) {
-      if (tc)
+      if (tc5)
+        SD_TRY(hgemm_tcgen05(ix->ht_tiled, hs.hq_tiled.ptr, ix->nks, ix->hpad, int(bm), kchunk / bkk, rows,
+                             hs.part.as<float>(), st));
+      else if (tc)
         hgemm_tf32x3_kernel<<<grid, 128, 0, st>>>(hs.hqt.as<float>(), static_cast<const float*>(ix->ht), K, hs.qpad,
                                                   ix->hpad, kchunk, ix->hpad, rows, hs.part.as<float>());
       else

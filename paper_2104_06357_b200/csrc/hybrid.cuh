@@ -14,12 +14,20 @@ struct HybridState {
   Scratch count;
   Scratch gcount;       // work counter of the dense gather
   Scratch hqt;          // [n_cols][qpad] dense heavy query rows
+  Scratch hq_tiled;     // the same rows as the tensor-core GEMM's B operand image
   Scratch part;         // GEMM K-split partials
   Scratch dqh;          // [qpad][hpad] heavy query x heavy index row sums
   Scratch dlh;          // [n][qpad] light index row x heavy query sums
 };
 
 int64_t hybrid_threshold(int64_t n_cols);
+// hgemm_tc.cu (fp32 tensor-core GEMM): operand images in the tiled UMMA
+// layout, then P[z][q][h] (q < rows) = sum over split z's K-steps (`per` each)
+int64_t tc_kstep();
+int tiled_operand(const sd_csr* m, const int32_t* rows, int64_t nrows, int R, int64_t nks, void* out,
+                  cudaStream_t st);
+int hgemm_tcgen05(const void* at, const void* bt, int64_t nks, int64_t hpad, int N, int64_t per, int64_t rows,
+                  float* part, cudaStream_t st);
 bool hybrid_enabled();
 bool hybrid_forced();
 // classify query rows, then GEMM + gather for the heavy ones (no-op when none)

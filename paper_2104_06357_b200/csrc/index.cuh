@@ -38,6 +38,8 @@ struct sd_index {
   int64_t heavy_deg = 0, n_heavy = 0, hpad = 0;
   int32_t* hid = nullptr;  // [n_rows]: heavy id or -1
   void* ht = nullptr;      // [n_cols][hpad] T: HT[c][h] = B[heavy row h][c]
+  void* ht_tiled = nullptr;  // fp32: HT as the tensor-core GEMM's A operand image (hgemm_tc.cu)
+  int64_t nks = 0;           // its K-steps of 32 columns
   int32_t* lrows = nullptr;  // [n_light] the other rows, by descending degree
   int64_t n_light = 0;
 };

@@ -372,7 +372,7 @@ DOT_FAMILY = ("cosine", "euclidean", "correlation", "dot", "dice", "jaccard", "h
 
 @pytest.mark.parametrize("dtype", DTYPES)
 def test_hybrid_heavy_rows_vs_oracle(dtype, monkeypatch):
-    """Hybrid path (hybrid.cu): query rows with >= n_cols/16 nonzeros are
+    """Hybrid path (hybrid.cu): query rows with >= max(64, n_cols/32) nonzeros are
     computed densely (GEMM against the index's heavy rows + gather over its
     light rows) and the sweep skips them.  Every dot-family metric against the
     oracle, and against the sweep-only path (SD_HYBRID=0) within rounding."""
@@ -380,7 +380,7 @@ def test_hybrid_heavy_rows_vs_oracle(dtype, monkeypatch):
     from paper_2104_06357_b200 import _lib
     idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
     deg = np.diff(np.asarray(idx.indptr))
-    heavy = np.flatnonzero(deg >= 100)
+    heavy = np.flatnonzero(deg >= max(64, -(-idx.n_cols // 32)))
     assert len(heavy) >= 64
     rows = np.sort(np.concatenate([heavy[:40], np.arange(0, idx.n_rows, 37)]))
     q = _gather_rows(idx, np.unique(rows))
