@@ -121,8 +121,12 @@ __global__ void __launch_bounds__(128) hgemm_tcgen05_kernel(const unsigned char*
   __shared__ __align__(8) unsigned long long bars[2 * 8 + 1];  // full[8], empty[8], done
   __shared__ uint32_t tmem_slot;
   const uint32_t full0 = uint32_t(__cvta_generic_to_shared(&bars[0])), empty0 = full0 + 64, done = full0 + 128;
+  // NACC accumulators used round-robin by K-step and summed at the end in
+  // IEEE fp32: the tensor core's fp32 accumulation is not round-to-nearest,
+  // so long single chains drift (1e-5 relative over ~400 steps on C2)
+  const int nacc = N <= 128 ? 4 : 2;
   uint32_t ncols = 32;
-  while (ncols < uint32_t(N)) ncols <<= 1;
+  while (ncols < uint32_t(nacc * N)) ncols <<= 1;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  :: "r"(uint32_t(__cvta_generic_to_shared(&tmem_slot))), "r"(ncols) : "memory");
@@ -161,12 +165,13 @@ __global__ void __launch_bounds__(128) hgemm_tcgen05_kernel(const unsigned char*
       const uint32_t sa = sbase + uint32_t(s) * stage_bytes;
       const uint32_t a_hi = sa, a_lo = sa + a_part, b_hi = sa + 2 * a_part, b_lo = b_hi + b_part;
 #pragma unroll
+      const uint32_t d = tmem + uint32_t(i % nacc) * uint32_t(N);
       for (int kk = 0; kk < TC_BK / 8; ++kk) {
         const uint32_t ao = uint32_t(kk) * TC_M * 32, bo = uint32_t(kk) * uint32_t(N) * 32;
-        const uint32_t first = (i == 0 && kk == 0) ? 0u : 1u;
-        mma_tf32(tmem, smem_desc(a_lo + ao), smem_desc(b_hi + bo), idesc, first);
-        mma_tf32(tmem, smem_desc(a_hi + ao), smem_desc(b_lo + bo), idesc, 1u);
-        mma_tf32(tmem, smem_desc(a_hi + ao), smem_desc(b_hi + bo), idesc, 1u);
+        const uint32_t first = (i < nacc && kk == 0) ? 0u : 1u;
+        mma_tf32(d, smem_desc(a_lo + ao), smem_desc(b_hi + bo), idesc, first);
+        mma_tf32(d, smem_desc(a_hi + ao), smem_desc(b_lo + bo), idesc, 1u);
+        mma_tf32(d, smem_desc(a_hi + ao), smem_desc(b_hi + bo), idesc, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                    :: "r"(empty0 + 8 * s) : "memory");
@@ -180,18 +185,26 @@ __global__ void __launch_bounds__(128) hgemm_tcgen05_kernel(const unsigned char*
   // epilogue: warp w owns TMEM lanes 32w..32w+31 = heavy rows h0 + 32w + lane
   float* out = P + int64_t(blockIdx.z) * rows * ldh;
   const int64_t h = int64_t(blockIdx.x) * TC_M + warp * 32 + lane;
+  const int used = int(tmin<int64_t>(nacc, nsteps));  // accumulators written at least once
   for (int c0 = 0; c0 < N; c0 += 16) {
-    uint32_t r[16];
-    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0);
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                   "=r"(r[15])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float sum[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sum[j] = 0.f;
+    for (int q = 0; q < used; ++q) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(q * N + c0);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                     "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                     "=r"(r[15])
+                   : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sum[j] = __fadd_rn(sum[j], __uint_as_float(r[j]));
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (c0 + j < rows) out[int64_t(c0 + j) * ldh + h] = nsteps > 0 ? __uint_as_float(r[j]) : 0.f;
+      if (c0 + j < rows) out[int64_t(c0 + j) * ldh + h] = sum[j];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -437,7 +437,7 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   const int64_t tiles_q = (hs.nhq + bm - 1) / bm, tiles_h = ix->hpad / bn;
   const int64_t rows = tiles_q * bm;  // GEMM rows computed (<= qpad)
   // K split so that the GEMM fills about two (tensor-core) or six waves of CTAs
-  const int64_t waves = tc5 ? 2 : 3 * 2;
+  const int64_t waves = tc5 ? 4 : 3 * 2;
   const int64_t want = std::max<int64_t>(1, (waves * int64_t(num_sms()) + tiles_q * tiles_h - 1) / (tiles_q * tiles_h));
   int64_t kchunk = (K + want - 1) / want;
   kchunk = std::max<int64_t>(bkk, (kchunk + bkk - 1) / bkk * bkk);
