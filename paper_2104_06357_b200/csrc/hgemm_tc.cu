@@ -77,14 +77,13 @@ int64_t tc_kstep() { return TC_BK; }
 __global__ void tiled_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                      const float* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
                                      int R, int64_t nks, unsigned char* __restrict__ out) {
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t part = uint32_t(R) * TC_BK * 4;
-  for (int64_t g = warp; g < nrows; g += nw) {
+  for (int64_t g = blockIdx.x; g < nrows; g += gridDim.x) {  // same (rows x chunks) grid as ht_scatter_kernel
     const int64_t r = rows[g];
     const int64_t tile = g / R;
     const int rr = int(g - tile * R);
-    for (int64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
+    const int64_t step = int64_t(gridDim.y) * blockDim.x;
+    for (int64_t e = ptr[r] + int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < ptr[r + 1]; e += step) {
       const int64_t k = idx[e];
       const float v = val[e];
       const uint32_t hi = tf32_bits(v);
@@ -217,8 +216,7 @@ int tiled_operand(const sd_csr* m, const int32_t* rows, int64_t nrows, int R, in
   const int64_t ntiles = (nrows + R - 1) / R;
   SD_CUDA_TRY(cudaMemsetAsync(out, 0, size_t(ntiles) * size_t(nks) * 2 * size_t(R) * TC_BK * 4, st));
   if (nrows == 0) return SD_OK;
-  const int blocks = int(std::min<int64_t>((nrows * 32 + 255) / 256, int64_t(num_sms()) * 8));
-  tiled_scatter_kernel<<<blocks, 256, 0, st>>>(m->indptr, m->indices, static_cast<const float*>(m->values), rows,
+  tiled_scatter_kernel<<<row_scatter_grid(nrows), 256, 0, st>>>(m->indptr, m->indices, static_cast<const float*>(m->values), rows,
                                                nrows, R, nks, static_cast<unsigned char*>(out));
   SD_LAUNCH_CHECK();
   return SD_OK;

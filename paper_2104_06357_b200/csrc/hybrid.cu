@@ -46,16 +46,25 @@ bool hybrid_forced() { return env_i64("SD_HYBRID", 1) == 2; }
 
 // ---------------------------------------------------------------- index side
 
+// dense[idx][h] = val for the nonzeros of rows[h]: block (h, c) of a
+// (rows x chunks) grid takes every chunks-th 256-wide slice of row rows[h], so
+// a handful of long rows still spreads over the whole GPU
 template <typename T>
 __global__ void ht_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                   const T* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
                                   int64_t pad, T* __restrict__ dense) {
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t h = warp; h < nrows; h += nw) {
+  for (int64_t h = blockIdx.x; h < nrows; h += gridDim.x) {
     const int64_t r = rows[h];
-    for (int64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) dense[int64_t(idx[e]) * pad + h] = val[e];
+    const int64_t step = int64_t(gridDim.y) * blockDim.x;
+    for (int64_t e = ptr[r] + int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < ptr[r + 1]; e += step)
+      dense[int64_t(idx[e]) * pad + h] = val[e];
   }
+}
+
+dim3 row_scatter_grid(int64_t nrows) {
+  const int64_t chunks = std::min<int64_t>(64, std::max<int64_t>(1, (int64_t(num_sms()) * 8 + nrows - 1) /
+                                                                        std::max<int64_t>(1, nrows)));
+  return dim3{unsigned(std::min<int64_t>(std::max<int64_t>(1, nrows), 65535)), unsigned(chunks), 1u};
 }
 
 int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st) {
@@ -90,9 +99,8 @@ int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st
   if (!light.empty())
     SD_CUDA_TRY(cudaMemcpyAsync(ix->lrows, light.data(), sizeof(int32_t) * light.size(), cudaMemcpyHostToDevice, st));
   SD_CUDA_TRY(cudaMemsetAsync(ix->ht, 0, dense_bytes, st));
-  const int blocks = int(std::min<int64_t>((nh * 32 + 255) / 256, int64_t(num_sms()) * 8));
   SD_TRY(SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
-    ht_scatter_kernel<T><<<blocks, 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
+    ht_scatter_kernel<T><<<row_scatter_grid(nh), 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
                                                   drows.as<int32_t>(), nh, pad, static_cast<T*>(ix->ht));
     SD_LAUNCH_CHECK();
     return SD_OK;
@@ -449,9 +457,8 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   SD_TRY(hs.part.alloc(es * size_t(splits) * size_t(rows) * size_t(ix->hpad), st));
   SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
   SD_TRY(hs.dlh.alloc(es * size_t(std::max<int64_t>(1, b->n_rows)) * size_t(hs.qpad), st));
-  const int gblocks = int(std::min<int64_t>((int64_t(hs.nhq) * 32 + 255) / 256, int64_t(num_sms()) * 8));
   return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
-    ht_scatter_kernel<T><<<gblocks, 256, 0, st>>>(a->indptr, a->indices, static_cast<const T*>(a->values),
+    ht_scatter_kernel<T><<<row_scatter_grid(hs.nhq), 256, 0, st>>>(a->indptr, a->indices, static_cast<const T*>(a->values),
                                                   hs.hq.as<int32_t>(), hs.nhq, hs.qpad, hs.hqt.as<T>());
     SD_LAUNCH_CHECK();
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};

@@ -24,6 +24,7 @@ int64_t hybrid_threshold(int64_t n_cols);
 // hgemm_tc.cu (fp32 tensor-core GEMM): operand images in the tiled UMMA
 // layout, then P[z][q][h] (q < rows) = sum over split z's K-steps (`per` each)
 int64_t tc_kstep();
+dim3 row_scatter_grid(int64_t nrows);  // grid of the per-row scatter kernels
 int tiled_operand(const sd_csr* m, const int32_t* rows, int64_t nrows, int R, int64_t nks, void* out,
                   cudaStream_t st);
 int hgemm_tcgen05(const void* at, const void* bt, int64_t nks, int64_t hpad, int N, int64_t per, int64_t rows,

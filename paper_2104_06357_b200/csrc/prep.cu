@@ -33,7 +33,11 @@ constexpr int STAT_CHUNK = 256;
 constexpr int64_t STAT_BLOCKED = 2048;  // longer rows: 32 lane-blocked partial sums
 constexpr int STAT_WARPS = 4;
 
-template <typename T, int KIND, int SR>
+// LONG = false: one lane per row, rows of <= STAT_LONG entries (all rows for
+// L0).  LONG = true: one warp per row, the longer rows — a second launch so
+// that the long rows of power-law data run side by side, not one after
+// another inside the warp that owns their 32-row group.
+template <typename T, int KIND, int SR, bool LONG>
 __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t* __restrict__ ptr,
                                                                    const T* __restrict__ val, int64_t n_rows,
                                                                    T p, T* __restrict__ out, T* __restrict__ out2) {
@@ -41,14 +45,17 @@ __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t
   const unsigned lane = lane_id();
   const int w = threadIdx.x >> 5;
   const int64_t nwarps = int64_t(gridDim.x) * STAT_WARPS;
-  for (int64_t r0 = (int64_t(blockIdx.x) * STAT_WARPS + w) * 32; r0 < n_rows; r0 += nwarps * 32) {
-    const int64_t r = r0 + lane;
-    const bool ok = r < n_rows;
+  const int64_t gwarp = int64_t(blockIdx.x) * STAT_WARPS + w;
+  for (int64_t r0 = LONG ? gwarp : gwarp * 32; r0 < n_rows; r0 += LONG ? nwarps : nwarps * 32) {
+    const int64_t r = LONG ? r0 : r0 + lane;
+    const bool ok = r < n_rows && (!LONG || lane == 0);
     const int64_t beg = ok ? ptr[r] : 0, end = ok ? ptr[r + 1] : 0;
+    const bool mine = LONG ? end - beg > STAT_LONG : (KIND == SD_STAT_L0 || end - beg <= STAT_LONG);
+    if (LONG && !__any_sync(0xffffffffu, ok && mine)) continue;
     T s = T(0);
     if constexpr (KIND == SD_STAT_L0) {
       s = T(end - beg);
-    } else if (end - beg <= STAT_LONG) {
+    } else if (!LONG && end - beg <= STAT_LONG) {
       int64_t e = beg;
       for (; e + 8 <= end; e += 8) {
         T t[8];
@@ -59,7 +66,7 @@ __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t
       }
       for (; e < end; ++e) s = add_rn(s, stat_term<T, KIND, SR>(__ldg(val + e), p));
     }
-    if constexpr (KIND != SD_STAT_L0) {
+    if constexpr (KIND != SD_STAT_L0 && LONG) {
       unsigned long_mask = __ballot_sync(0xffffffffu, ok && end - beg > STAT_LONG);
       while (long_mask) {
         const int src = __ffs(long_mask) - 1;
@@ -118,9 +125,9 @@ __global__ void __launch_bounds__(STAT_WARPS * 32) row_stat_kernel(const int64_t
         ls = __shfl_sync(0xffffffffu, ls, 0);
         if (int(lane) == src) s = ls;
       }
-      if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
     }
-    if (ok) {
+    if constexpr (KIND == SD_STAT_L2) s = sqrt_rn(s);
+    if (ok && mine) {
       out[r] = s;
       if constexpr (KIND == SD_STAT_L2)  // optional 1/||row|| (0 for empty rows), same pass
         if (out2) out2[r] = s > T(0) ? div_rn(T(1), s) : T(0);
@@ -133,9 +140,15 @@ static int launch_stat(const sd_csr* m, T p, void* out, cudaStream_t st, void* o
   if (m->n_rows == 0) return SD_OK;
   const int64_t warps = (m->n_rows + 31) / 32;
   int blocks = int(tmin<int64_t>((warps + STAT_WARPS - 1) / STAT_WARPS, int64_t(num_sms()) * 16));
-  row_stat_kernel<T, KIND, SR><<<blocks, STAT_WARPS * 32, 0, st>>>(
+  row_stat_kernel<T, KIND, SR, false><<<blocks, STAT_WARPS * 32, 0, st>>>(
       m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out), static_cast<T*>(out2));
   SD_LAUNCH_CHECK();
+  if constexpr (KIND != SD_STAT_L0) {
+    const int lblocks = int(tmin<int64_t>((m->n_rows + STAT_WARPS - 1) / STAT_WARPS, int64_t(num_sms()) * 32));
+    row_stat_kernel<T, KIND, SR, true><<<lblocks, STAT_WARPS * 32, 0, st>>>(
+        m->indptr, static_cast<const T*>(m->values), m->n_rows, p, static_cast<T*>(out), static_cast<T*>(out2));
+    SD_LAUNCH_CHECK();
+  }
   return SD_OK;
 }
 
