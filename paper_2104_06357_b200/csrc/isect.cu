@@ -214,16 +214,22 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
   __shared__ unsigned int hist[64];
   __shared__ unsigned int base[64];
   __shared__ unsigned long long total;
-  __shared__ int64_t part[1024];
   if (threadIdx.x < 64) hist[threadIdx.x] = 0;
   if (threadIdx.x == 0) total = 0;
   __syncthreads();
+  // degree buckets with warp-aggregated shared atomics (power-law queries
+  // crowd a few buckets: one atomic per distinct bucket in the warp)
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt = (1u << lane) - 1u;
   unsigned long long local = 0;
-  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
-    const int64_t d = ptr[r + 1] - ptr[r];
+  for (int64_t r0 = 0; r0 < m; r0 += blockDim.x) {  // warp-uniform trip count
+    const int64_t r = r0 + threadIdx.x;
+    const bool ok = r < m;
+    const int64_t d = ok ? ptr[r + 1] - ptr[r] : 0;
     const int b = d > 0 ? 63 - __clzll(d) : 0;
-    atomicAdd(&hist[63 - b], 1u);
-    if (!skip || skip[r] < 0) local += (unsigned long long)(d + epi_cost);
+    const unsigned grp = __match_any_sync(0xffffffffu, ok ? unsigned(63 - b) : 64u + lane);
+    if (ok && (grp & lt) == 0u) atomicAdd(&hist[63 - b], unsigned(__popc(grp)));
+    if (ok && (!skip || skip[r] < 0)) local += (unsigned long long)(d + epi_cost);
   }
   atomicAdd(&total, local);
   __syncthreads();
@@ -232,10 +238,17 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     for (int b = 0; b < 64; ++b) { base[b] = acc; acc += hist[b]; }
   }
   __syncthreads();
-  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
-    const int64_t d = ptr[r + 1] - ptr[r];
+  for (int64_t r0 = 0; r0 < m; r0 += blockDim.x) {
+    const int64_t r = r0 + threadIdx.x;
+    const bool ok = r < m;
+    const int64_t d = ok ? ptr[r + 1] - ptr[r] : 0;
     const int b = d > 0 ? 63 - __clzll(d) : 0;
-    order[atomicAdd(&base[63 - b], 1u)] = int32_t(r);
+    const unsigned grp = __match_any_sync(0xffffffffu, ok ? unsigned(63 - b) : 64u + lane);
+    const int leader = __ffs(grp) - 1;
+    unsigned pos0 = 0;
+    if (ok && int(lane) == leader) pos0 = atomicAdd(&base[63 - b], unsigned(__popc(grp)));
+    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    if (ok) order[pos0 + __popc(grp & lt)] = int32_t(r);
   }
   __syncthreads();
   if (tile_major) {  // items (tile t, position p) ordered tile-major: item = t * m + p
@@ -256,15 +269,15 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     tpi[q] = int32_t(t);
     if (!skip || skip[r] < 0) sum += (band + t - 1) / t;  // rows of the hybrid path get no items
   }
-  part[threadIdx.x] = sum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int t = 0; t < int(blockDim.x); ++t) { const int64_t v = part[t]; part[t] = acc; acc += v; }
-    item_off[m] = acc;
+  // block-wide exclusive scan of the per-thread item counts
+  int64_t off;
+  {
+    typedef cub::BlockScan<int64_t, 1024> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    int64_t total_items;
+    Scan(scan_tmp).ExclusiveSum(sum, off, total_items);
+    if (threadIdx.x == 0) item_off[m] = total_items;
   }
-  __syncthreads();
-  int64_t off = part[threadIdx.x];
   for (int64_t q = lo; q < hi; ++q) {
     item_off[q] = off;
     const int64_t cnt = (skip && skip[order[q]] >= 0) ? 0 : (band + tpi[q] - 1) / tpi[q];

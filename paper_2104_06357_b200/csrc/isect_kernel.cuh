@@ -642,11 +642,24 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
     const int64_t j0 = blk * JB;
     const int jn = int(tmin<int64_t>(JB, a.n - j0));
     __syncthreads();
-    for (int64_t e = threadIdx.x; e < int64_t(jn) * qpad; e += blockDim.x) {
-      const int64_t jj = e / qpad;
-      sv[jj * qs + (e - jj * qpad)] = dlh[j0 * qpad + e];
+    const int qp = int(qpad);
+    for (int e = threadIdx.x; e < jn * qp; e += blockDim.x) {
+      const int jj = e / qp;
+      sv[jj * qs + (e - jj * qp)] = dlh[j0 * qpad + e];
     }
     __syncthreads();
+    // per-cell index-row data, loaded once per block row instead of once per heavy query
+    constexpr int JL = 2;  // cells per lane (JB <= 64)
+    int32_t hj[JL];
+    T gb0[JL], gb1[JL];
+#pragma unroll
+    for (int u = 0; u < JL; ++u) {
+      const int jj = lane + 32 * u;
+      const bool ok = jj < jn;
+      hj[u] = ok ? hid[j0 + jj] : -1;
+      gb0[u] = ok && a.sb0 ? a.sb0[j0 + jj] : T(0);
+      gb1[u] = ok && a.sb1 ? a.sb1[j0 + jj] : T(0);
+    }
     for (int qq = warp; qq < nhq; qq += int(blockDim.x >> 5)) {
       const int64_t i = hq[qq];
       const T ra0 = a.sa0 ? a.sa0[i] : T(0);
@@ -654,15 +667,16 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
       bool fast_zero;
       T zero_val;
       isect_zero<T, M>(a, ra0, ra1, fast_zero, zero_val);
-      for (int jj = lane; jj < jn; jj += 32) {
-        const int64_t j = j0 + jj;
-        const int32_t h = hid[j];
-        const T gv = h >= 0 ? dqh[int64_t(qq) * hpad + h] : sv[jj * qs + qq];
-        const T gb0 = a.sb0 ? a.sb0[j] : T(0);
-        const T gb1 = a.sb1 ? a.sb1[j] : T(0);
-        uint32_t f = 0;
-        __stcs(a.out + i * a.ldo + j, isect_cell<T, M>(a, gv, T(0), ra0, ra1, gb0, gb1, fast_zero, zero_val, f));
-        flags |= f;
+#pragma unroll
+      for (int u = 0; u < JL; ++u) {
+        const int jj = lane + 32 * u;
+        if (jj < jn) {
+          const T gv = hj[u] >= 0 ? dqh[int64_t(qq) * hpad + hj[u]] : sv[jj * qs + qq];
+          uint32_t f = 0;
+          __stcs(a.out + i * a.ldo + j0 + jj,
+                 isect_cell<T, M>(a, gv, T(0), ra0, ra1, gb0[u], gb1[u], fast_zero, zero_val, f));
+          flags |= f;
+        }
       }
     }
   }
@@ -679,7 +693,7 @@ int launch_heavy_rows(IsectArgs<T>& a, const int32_t* hq, int nhq, const int32_t
     return SD_E_UNSUPPORTED;
   } else {
     const int64_t per_row = (qpad + 1) * int64_t(sizeof(T));
-    const int JB = int(tmin<int64_t>(64, (smem_optin_bytes() - 4096) / per_row));
+    const int JB = int(tmin<int64_t>(64, (smem_optin_bytes() - 4096) / per_row));  // <= 2 cells per lane
     if (JB < 1) { set_error("too many heavy query rows for the hybrid epilogue"); return SD_E_INVALID; }
     const size_t smem = size_t(JB) * size_t(per_row);
     SD_TRY(prepare_smem(heavy_rows_kernel<T, M>, smem, "heavy_rows_kernel"));
