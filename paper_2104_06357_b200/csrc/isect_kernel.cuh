@@ -69,12 +69,14 @@ __device__ __forceinline__ double from_mask(uint32_t m, double) { return double(
 constexpr int EPF = SD_ISECT_EPF;
 
 // warps per CTA (one CTA per SM: 14 x 16 KB accumulators = 224 KB); capping
-// the CTA at 448 threads gives each thread up to 144 registers
+// the CTA at 448 threads (4 warps on some SM sub-partitions) caps each thread at 128 registers
 constexpr int ISECT_MAX_WARPS = 14;
 
-// columns whose first 32 postings are loaded before any is applied
+// columns whose first 32 postings are loaded before any is applied (16: half
+// the code and the registers of 32 and measured faster on C2/C3/C5 — the
+// kernel is large enough for instruction-cache misses to show)
 #ifndef SD_ISECT_U32
-#define SD_ISECT_U32 32
+#define SD_ISECT_U32 16
 #endif
 template <typename T> struct IsectU { static constexpr int value = sizeof(T) == 4 ? SD_ISECT_U32 : 16; };
 
