@@ -64,7 +64,7 @@ __device__ __forceinline__ double from_mask(uint32_t m, double) { return double(
 
 // fast epilogue: 128-cell groups in flight per warp
 #ifndef SD_ISECT_EPF
-#define SD_ISECT_EPF 2
+#define SD_ISECT_EPF 4
 #endif
 constexpr int EPF = SD_ISECT_EPF;
 
