@@ -399,3 +399,19 @@ def test_hybrid_heavy_rows_vs_oracle(dtype, monkeypatch):
         monkeypatch.setenv("SD_HYBRID", "2")
         assert_parity(got, sweep, a, b, name, dtype, what=f"hybrid vs sweep/{name}")
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n_heavy_q", [17, 300])
+def test_hybrid_gemm_routes(n_heavy_q, monkeypatch):
+    """The heavy block's GEMM: tcgen05 (<= 256 heavy queries, N = 32 here) and
+    the mma.sync fallback (> 256), both against the oracle (fp32)."""
+    idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
+    deg = np.diff(np.asarray(idx.indptr))
+    heavy = np.flatnonzero(deg >= max(64, -(-idx.n_cols // 32)))
+    q = _gather_rows(idx, np.sort(heavy[:n_heavy_q]))
+    monkeypatch.setenv("SD_HYBRID", "2")
+    for name in ("cosine", "euclidean"):
+        a, b = _host(q), _host(idx)
+        got = sd.pairwise_distances(a, b, sd.metric_registry(name), dtype=np.float32)
+        ref = O.pairwise_distances(a, b, name)
+        assert_parity(got, ref, a, b, name, np.float32, what=f"hybrid gemm {n_heavy_q}/{name}")
