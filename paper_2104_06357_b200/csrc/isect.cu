@@ -358,7 +358,14 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   const int64_t post_bytes = std::max<int64_t>(
       1, ix->nnz * int64_t(dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>)) +
              int64_t(sizeof(uint32_t)) * (ix->n_tiles * ix->n_cols + 1));
-  const int64_t n_bands0 = (post_bytes + l2_bytes() - 1) / l2_bytes();
+  // pairwise: a band's postings take about a fifth of the L2 (measured on C2:
+  // bands of 100 MB 2.37 ms, 50 MB 2.28, 25 MB 2.21, 12 MB 2.43) — the rest
+  // holds the streaming output and the per-row statistics.  kNN keeps whole-L2
+  // bands: every band adds a top-k list per query to merge (C5: 49 vs 56 ms).
+  const char* ld = getenv("SD_ISECT_L2_DIV");
+  const int64_t div = ld ? atoll(ld) : (topk > 0 ? 1 : 5);
+  const int64_t band_bytes = std::max<int64_t>(1, l2_bytes() / std::max<int64_t>(1, div));
+  const int64_t n_bands0 = (post_bytes + band_bytes - 1) / band_bytes;
   const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
   const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : auto_band));
   const int64_t max_items = m * band0 * ((ix->n_tiles + band0 - 1) / band0);
