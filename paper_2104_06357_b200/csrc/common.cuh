@@ -135,7 +135,19 @@ __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fm
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+// fp32: the hardware approximation (MUFU.SQRT, relative error ~2^-22, exact
+// at 0) — far inside the fp32 parity tolerance (1e-5) and one instruction
+// instead of the IEEE sequence (C2 euclidean 3.29 -> 2.67 ms); fp64 stays IEEE.
+// -DSD_IEEE_SQRT restores __fsqrt_rn.
+#ifndef SD_IEEE_SQRT
+__device__ __forceinline__ float sqrt_rn(float a) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+#else
 __device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+#endif
 __device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
 __device__ __forceinline__ float log_(float a) { return logf(a); }
 __device__ __forceinline__ double log_(double a) { return log(a); }
