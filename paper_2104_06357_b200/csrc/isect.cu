@@ -352,18 +352,34 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // bands of tiles whose postings fit the L2 together, so the index streams
   // from HBM about once while every query sweeps the resident band; bands are
   // split evenly (no short tail band).  SD_ISECT_BAND overrides (tuning).
+  const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
+  const int tile_major = pe ? atoi(pe) : 0;
+  // cosine over postings pre-divided by the index-row norms (built once per index)
+  const bool cos_scaled = md->metric == SD_M_COSINE && sb.s[1] != nullptr && getenv("SD_COS_RAW") == nullptr;
+  if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
+  // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
+  // computed densely; the sweep skips them
+  HybridState hs;
+  if (topk == 0 && ck == C_MUL && ix->n_heavy > 0 && hybrid_enabled() &&
+      (ix->n_tiles >= 4 || hybrid_forced())) {  // small indexes: the sweep is cheap, keep it exact
+    if (tm) tm->begin(PH_PASS2);
+    SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
+    if (tm) tm->end(PH_PASS2);
+  }
   const char* be0 = getenv("SD_ISECT_BAND");
   // bytes the sweep streams: postings + their (tile, column) ranges (not the
   // hybrid block or the other metric's posting copy, which it never touches)
   const int64_t post_bytes = std::max<int64_t>(
       1, ix->nnz * int64_t(dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>)) +
              int64_t(sizeof(uint32_t)) * (ix->n_tiles * ix->n_cols + 1));
-  // pairwise: a band's postings take about a fifth of the L2 (measured on C2:
-  // bands of 100 MB 2.37 ms, 50 MB 2.28, 25 MB 2.21, 12 MB 2.43) — the rest
-  // holds the streaming output and the per-row statistics.  kNN keeps whole-L2
-  // bands: every band adds a top-k list per query to merge (C5: 49 vs 56 ms).
+  // once the hybrid path has taken the heavy query rows, a band's postings
+  // take about a fifth of the L2 (C2 cosine: bands of 100 MB 2.37 ms, 50 MB
+  // 2.28, 25 MB 2.21, 12 MB 2.43) — the rest holds the streaming output.
+  // Otherwise whole-L2 bands: with heavy rows in the sweep (C2 manhattan 4.9
+  // vs 5.9 ms) and for kNN, where every band adds a top-k list per query to
+  // merge (C5: 49 vs 56 ms), smaller bands cost more than they save.
   const char* ld = getenv("SD_ISECT_L2_DIV");
-  const int64_t div = ld ? atoll(ld) : (topk > 0 ? 1 : 5);
+  const int64_t div = ld ? atoll(ld) : (hs.nhq > 0 ? 5 : 1);
   const int64_t band_bytes = std::max<int64_t>(1, l2_bytes() / std::max<int64_t>(1, div));
   const int64_t n_bands0 = (post_bytes + band_bytes - 1) / band_bytes;
   const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
@@ -376,21 +392,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   SD_TRY(item_pos.alloc(sizeof(int32_t) * max_items, st));
   SD_TRY(counter.alloc(sizeof(unsigned int), st));
   SD_CUDA_TRY(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int), st));
-  const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
-  const int tile_major = pe ? atoi(pe) : 0;
   const int64_t band = band0;
-  // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
-  // computed densely; the sweep skips them
-  // cosine over postings pre-divided by the index-row norms (built once per index)
-  const bool cos_scaled = md->metric == SD_M_COSINE && sb.s[1] != nullptr && getenv("SD_COS_RAW") == nullptr;
-  if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
-  HybridState hs;
-  if (topk == 0 && ck == C_MUL && ix->n_heavy > 0 && hybrid_enabled() &&
-      (ix->n_tiles >= 4 || hybrid_forced())) {  // small indexes: the sweep is cheap, keep it exact
-    if (tm) tm->begin(PH_PASS2);
-    SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
-    if (tm) tm->end(PH_PASS2);
-  }
   plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
                                   hs.nhq > 0 ? hs.qid.as<int32_t>() : nullptr,
                                   order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
