@@ -115,11 +115,15 @@ template <> struct Num<float> {
   __device__ __forceinline__ static float inf() { return __int_as_float(0x7f800000); }
   __device__ __forceinline__ static float big() { return __int_as_float(0x7f800000); }  // KL saturation (1e308 not representable)
   __device__ __forceinline__ static float eps() { return FLT_EPSILON; }
+  __device__ __forceinline__ static float min_normal() { return FLT_MIN; }
+  __device__ __forceinline__ static float max_finite() { return FLT_MAX; }
 };
 template <> struct Num<double> {
   __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000ULL); }
   __device__ __forceinline__ static double big() { return 1e308; }  // KL_SATURATION, metrics.py:29
   __device__ __forceinline__ static double eps() { return DBL_EPSILON; }
+  __device__ __forceinline__ static double min_normal() { return DBL_MIN; }
+  __device__ __forceinline__ static double max_finite() { return DBL_MAX; }
 };
 
 // Exact IEEE ops, spelled out so that no FMA contraction can change the

@@ -140,8 +140,8 @@ __device__ __forceinline__ T contrib(T a, T b, T p) {
                      : CK == C_CANBERRA ? SD_SR_CANBERRA
                      : CK == C_MISMATCH ? SD_SR_MISMATCH : SD_SR_JS_TERM;
     const T both = product<SR, T>(a, b, p);
-    const T left = product<SR, T>(a, T(0), p);
-    const T right = product<SR, T>(T(0), b, p);
+    const T left = product_a0<SR, T>(a, p);
+    const T right = product_0b<SR, T>(b, p);
     return sub_rn(sub_rn(both, left), right);
   }
 }

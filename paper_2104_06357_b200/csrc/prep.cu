@@ -17,8 +17,8 @@ __device__ __forceinline__ T stat_term(T v, T p) {
   else if constexpr (KIND == SD_STAT_L1) return abs_(v);
   else if constexpr (KIND == SD_STAT_L2 || KIND == SD_STAT_L2SQ) return mul_rn(v, v);
   else if constexpr (KIND == SD_STAT_SUM) return v;
-  else if constexpr (KIND == STAT_ONESIDED_A) return product<SR, T>(v, T(0), p);
-  else return product<SR, T>(T(0), v, p);  // STAT_ONESIDED_B
+  else if constexpr (KIND == STAT_ONESIDED_A) return product_a0<SR, T>(v, p);
+  else return product_0b<SR, T>(v, p);  // STAT_ONESIDED_B
 }
 
 // Sequential ascending sums (the association order of the fused kernel's

@@ -91,6 +91,30 @@ __device__ __forceinline__ T warp_reduce(T v) {
   return v;
 }
 
+// One-sided terms ⊗(x, 0) and ⊗(0, y) of a single stored entry (the union
+// decomposition's correction terms and one-sided row sums).  The JS term
+// reduces to x·log 2 whenever x/2 is exact (normal x): the same value as the
+// general formula (mu = x/2, x/mu == 2) without its division and log.
+// Canberra's is |x| / |x| = 1 exactly for any finite non-zero x.
+template <int SR, typename T>
+__device__ __forceinline__ T product_a0(T x, T p) {
+  if constexpr (SR == SD_SR_JS_TERM) {
+    if (x >= T(2) * Num<T>::min_normal()) return mul_rn(x, log_(T(2)));
+  } else if constexpr (SR == SD_SR_CANBERRA) {
+    if (x != T(0) && abs_(x) <= Num<T>::max_finite()) return T(1);
+  }
+  return product<SR, T>(x, T(0), p);
+}
+template <int SR, typename T>
+__device__ __forceinline__ T product_0b(T y, T p) {
+  if constexpr (SR == SD_SR_JS_TERM) {
+    if (y >= T(2) * Num<T>::min_normal()) return mul_rn(y, log_(T(2)));
+  } else if constexpr (SR == SD_SR_CANBERRA) {
+    if (y != T(0) && abs_(y) <= Num<T>::max_finite()) return T(1);
+  }
+  return product<SR, T>(T(0), y, p);
+}
+
 }  // namespace sd
 
 #define SD_DISPATCH_SEMIRING(sr, SR, ...)                                          \
