@@ -262,12 +262,29 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
   const int64_t chunk = (m + blockDim.x - 1) / blockDim.x;
   const int64_t lo = tmin<int64_t>(m, int64_t(threadIdx.x) * chunk), hi = tmin<int64_t>(m, lo + chunk);
   int64_t sum = 0;
-  for (int64_t q = lo; q < hi; ++q) {
-    const int64_t r = order[q];
-    const int64_t cost = ptr[r + 1] - ptr[r] + epi_cost;
-    const int64_t t = tmin<int64_t>(band, tmax<int64_t>(1, target / cost));
-    tpi[q] = int32_t(t);
-    if (!skip || skip[r] < 0) sum += (band + t - 1) / t;  // rows of the hybrid path get no items
+  // 8 positions at a time: their row ids, then their degrees, are loaded
+  // together (one round trip each instead of one per position); the item
+  // count of each position is parked in item_off until the scan
+  for (int64_t q0 = lo; q0 < hi; q0 += 8) {
+    int64_t r[8], d[8];
+    bool sk[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r[u] = q0 + u < hi ? order[q0 + u] : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      d[u] = q0 + u < hi ? ptr[r[u] + 1] - ptr[r[u]] : 0;
+      sk[u] = q0 + u < hi && skip && skip[r[u]] >= 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (q0 + u < hi) {
+        const int64_t t = tmin<int64_t>(band, tmax<int64_t>(1, target / (d[u] + epi_cost)));
+        const int64_t cnt = sk[u] ? 0 : (band + t - 1) / t;  // rows of the hybrid path get no items
+        tpi[q0 + u] = int32_t(t);
+        item_off[q0 + u] = cnt;
+        sum += cnt;
+      }
+    }
   }
   // block-wide exclusive scan of the per-thread item counts
   int64_t off;
@@ -279,8 +296,8 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
     if (threadIdx.x == 0) item_off[m] = total_items;
   }
   for (int64_t q = lo; q < hi; ++q) {
+    const int64_t cnt = item_off[q];
     item_off[q] = off;
-    const int64_t cnt = (skip && skip[order[q]] >= 0) ? 0 : (band + tpi[q] - 1) / tpi[q];
     for (int64_t it = 0; it < cnt; ++it) item_pos[off + it] = int32_t(q);
     off += cnt;
   }
