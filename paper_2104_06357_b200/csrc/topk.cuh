@@ -23,6 +23,8 @@ template <typename T, int KPL>
 struct WarpTopK {
   T d[KPL];
   int64_t i[KPL];
+  T thr_d;          // the k-th entry, refreshed after every insertion (rare):
+  int64_t thr_i;    // the common offer is a compare and a vote, no shuffles
 
   __device__ __forceinline__ void init() {
 #pragma unroll
@@ -30,6 +32,8 @@ struct WarpTopK {
       d[s] = T(NAN);
       i[s] = INT64_MAX;
     }
+    thr_d = T(NAN);
+    thr_i = INT64_MAX;
   }
 
   // current k-th entry (the admission threshold)
@@ -73,10 +77,10 @@ struct WarpTopK {
 
   // offer one candidate per lane (valid lanes only), in lane order
   __device__ __forceinline__ void offer(bool valid, T cd, int64_t ci, int k) {
-    T td;
-    int64_t ti;
-    kth(k, td, ti);
+    const T td = thr_d;
+    const int64_t ti = thr_i;
     unsigned mask = __ballot_sync(0xffffffffu, valid && key_less(cd, ci, td, ti));
+    const bool inserted = mask != 0u;
     while (mask) {
       const int src = __ffs(mask) - 1;
       mask &= mask - 1;
@@ -84,6 +88,7 @@ struct WarpTopK {
       const int64_t si = __shfl_sync(0xffffffffu, ci, src);
       insert(sd_, si, k);
     }
+    if (inserted) kth(k, thr_d, thr_i);
   }
 
   __device__ __forceinline__ void store(int k, T* od, int64_t* oi, int64_t base) const {
