@@ -18,6 +18,7 @@
 // sparse intersection sums up to rounding (products with an absent entry are
 // exact zeros).
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <cstdlib>
 #include <vector>
@@ -137,6 +138,18 @@ void hybrid_index_free(sd_index* ix) {
 }
 
 // ---------------------------------------------------------------- query side
+
+// one non-blocking side stream per device (created once, never destroyed)
+cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
+    streams[dev] = nullptr;
+  return streams[dev];
+}
 
 // heavy query rows get ids 0..cap-1 (the id order is irrelevant to results:
 // every heavy row is computed independently of its slot)
@@ -461,6 +474,28 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     ht_scatter_kernel<T><<<row_scatter_grid(hs.nhq), 256, 0, st>>>(a->indptr, a->indices, static_cast<const T*>(a->values),
                                                   hs.hq.as<int32_t>(), hs.nhq, hs.qpad, hs.hqt.as<T>());
     SD_LAUNCH_CHECK();
+    // the dense gather only needs HQT: it runs on a side stream, overlapping
+    // the tensor-core GEMM (different bottlenecks: L2 latency vs tensor pipe /
+    // TMA) and whatever of the sweep it can share SMs with; heavy_rows joins
+    cudaStream_t side = side_stream();
+    if (!side) side = st;
+    if (side != st) {
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.fork, st));
+      SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
+    }
+    const int64_t nblk = hs.qpad / 128;
+    int per_sm = 0;
+    SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T>, 256, 0));
+    hgather_kernel<T><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
+        b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hs.qpad,
+        nblk, int64_t(hs.nhq), hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+    SD_LAUNCH_CHECK();
+    if (side != st) {
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.join, side));
+      hs.main = st;
+    }
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
     if constexpr (sizeof(T) == 4) {
       if (tc5)
@@ -481,12 +516,6 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     hreduce_kernel<T><<<int(std::min<int64_t>((count + 255) / 256, int64_t(num_sms()) * 16)), 256, 0, st>>>(
         hs.part.as<T>(), int(splits), count, hs.dqh.as<T>());
     SD_LAUNCH_CHECK();
-    const int64_t nblk = hs.qpad / 128;
-    int per_sm = 0;
-    SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T>, 256, 0));
-    hgather_kernel<T><<<std::max(1, per_sm) * num_sms(), 256, 0, st>>>(
-        b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hs.qpad,
-        nblk, int64_t(hs.nhq), hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
     SD_LAUNCH_CHECK();
     return SD_OK;
   });

@@ -7,6 +7,20 @@ struct sd_index;
 namespace sd {
 
 struct HybridState {
+  cudaEvent_t fork = nullptr;  // the gather's side-stream fork / join (hybrid_prepare)
+  cudaEvent_t join = nullptr;
+  cudaStream_t main = nullptr;  // the caller's stream (scratch below is freed on it)
+  // the caller's stream waits for the side stream (before heavy_rows and
+  // before any of this state's scratch is released on it)
+  int wait(cudaStream_t st) {
+    if (join && cudaStreamWaitEvent(st, join, 0) != cudaSuccess) return SD_E_CUDA;
+    return SD_OK;
+  }
+  ~HybridState() {  // runs before the Scratch members free their buffers on `main`
+    if (join && main) cudaStreamWaitEvent(main, join, 0);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
   int nhq = 0;          // heavy query rows of this call (ids 0..nhq-1)
   int64_t qpad = 0;     // nhq rounded up to 128
   Scratch qid;          // [m] heavy id of each query row or -1

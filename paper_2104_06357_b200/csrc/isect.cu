@@ -454,7 +454,8 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     SD_TRY(isect_launch(args, md->metric, W, st));
     if (tm) tm->end(PH_PASS1);
     if (hs.nhq > 0) {
-      if (tm) tm->begin(PH_EXPANSION);
+      if (tm) tm->begin(PH_EXPANSION);  // includes any wait for the side-stream gather
+      SD_TRY(hs.wait(st));
       SD_TRY(isect_heavy_rows(args, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(), ix->hpad,
                               hs.dlh.as<T>(), hs.qpad, st));
       if (tm) tm->end(PH_EXPANSION);
