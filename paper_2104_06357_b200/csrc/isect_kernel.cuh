@@ -70,7 +70,10 @@ constexpr int EPF = SD_ISECT_EPF;
 
 // warps per CTA (one CTA per SM: 14 x 16 KB accumulators = 224 KB); capping
 // the CTA at 448 threads (4 warps on some SM sub-partitions) caps each thread at 128 registers
-constexpr int ISECT_MAX_WARPS = 14;
+#ifndef SD_ISECT_WARPS
+#define SD_ISECT_WARPS 14
+#endif
+constexpr int ISECT_MAX_WARPS = SD_ISECT_WARPS;
 
 // columns whose first 32 postings are loaded before any is applied (16: half
 // the code and the registers of 32 and measured faster on C2/C3/C5 — the
