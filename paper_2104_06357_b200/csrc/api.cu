@@ -143,10 +143,13 @@ static int fused_run(const sd_csr* a, const sd_csr* b, const sd_index* index, in
   Stats sa, sb;
   const int ph_stats = is_namm(md->metric) ? PH_PASS2 : PH_NORMS;
   tm.begin(ph_stats);
-  int rc = isect_stats(a, b, ix, dtype, md, sabuf, sbbuf, &sa, &sb, st);
+  // dot-family metrics that may take the hybrid path compute their query
+  // statistics inside isect_run (overlapped with the dense path)
+  const bool defer_a = isect_hybrid_eligible(ix, md, topk) && metric_stats_count(md->metric) > 0;
+  int rc = isect_stats(a, b, ix, dtype, md, sabuf, sbbuf, &sa, &sb, defer_a, st);
   tm.end(ph_stats);
   if (rc == SD_OK) {
-    rc = isect_run(a, b, ix, dtype, md, sa, sb, out, ldo, topk, base, out_d, out_i, flags, &tm, st);
+    rc = isect_run(a, b, ix, dtype, md, sa, sb, out, ldo, topk, base, out_d, out_i, flags, &tm, defer_a, st);
   }
   if (own) {
     cudaStreamSynchronize(st);

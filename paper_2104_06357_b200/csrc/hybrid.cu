@@ -139,16 +139,17 @@ void hybrid_index_free(sd_index* ix) {
 
 // ---------------------------------------------------------------- query side
 
-// one non-blocking side stream per device (created once, never destroyed)
-cudaStream_t side_stream() {
+// non-blocking side streams per device (created once, never destroyed):
+// 0 carries the dense gather, 1 the deferred query statistics
+cudaStream_t side_stream(int which) {
   static std::mutex mu;
-  static cudaStream_t streams[64] = {};
+  static cudaStream_t streams[2][64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (which < 0 || which > 1 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
-    streams[dev] = nullptr;
-  return streams[dev];
+  cudaStream_t& s = streams[which][dev];
+  if (!s && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
+  return s;
 }
 
 // heavy query rows get ids 0..cap-1 (the id order is irrelevant to results:
@@ -477,7 +478,7 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     // the dense gather only needs HQT: it runs on a side stream, overlapping
     // the tensor-core GEMM (different bottlenecks: L2 latency vs tensor pipe /
     // TMA) and whatever of the sweep it can share SMs with; heavy_rows joins
-    cudaStream_t side = side_stream();
+    cudaStream_t side = side_stream(0);
     if (!side) side = st;
     if (side != st) {
       SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));

@@ -10,6 +10,7 @@ struct HybridState {
   cudaEvent_t fork = nullptr;  // the gather's side-stream fork / join (hybrid_prepare)
   cudaEvent_t join = nullptr;
   cudaStream_t main = nullptr;  // the caller's stream (scratch below is freed on it)
+  cudaEvent_t stats_done = nullptr;  // deferred query statistics (isect_run) finished
   // the caller's stream waits for the side stream (before heavy_rows and
   // before any of this state's scratch is released on it)
   int wait(cudaStream_t st) {
@@ -19,6 +20,7 @@ struct HybridState {
   ~HybridState() {  // runs before the Scratch members free their buffers on `main`
     if (join && main) cudaStreamWaitEvent(main, join, 0);
     if (fork) cudaEventDestroy(fork);
+    if (stats_done) cudaEventDestroy(stats_done);
     if (join) cudaEventDestroy(join);
   }
   int nhq = 0;          // heavy query rows of this call (ids 0..nhq-1)
@@ -35,6 +37,7 @@ struct HybridState {
 };
 
 int64_t hybrid_threshold(int64_t n_cols);
+cudaStream_t side_stream(int which);  // per-device side streams (nullptr if unavailable)
 // hgemm_tc.cu (fp32 tensor-core GEMM): operand images in the tiled UMMA
 // layout, then P[z][q][h] (q < rows) = sum over split z's K-steps (`per` each)
 int64_t tc_kstep();

@@ -305,8 +305,13 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
 
 // Per-row statistics of both sides for the fused epilogue (norms for the
 // dot family, one-sided sums for NAMM metrics, degrees of A for KL).
+bool isect_hybrid_eligible(const sd_index* ix, const sd_metric_desc* md, int topk) {
+  return topk == 0 && metric_contrib(md->metric) == C_MUL && ix && ix->n_heavy > 0 && hybrid_enabled() &&
+         (ix->n_tiles >= 4 || hybrid_forced());  // small indexes: the sweep is cheap, keep it exact
+}
+
 int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtype, const sd_metric_desc* md,
-                Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st) {
+                Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, bool defer_a, cudaStream_t st) {
   const size_t es = dtype == SD_F64 ? 8 : 4;
   if (md->metric == SD_M_CHEBYSHEV) {  // top-K |a| per query row + per-entry ranks; B side lives in the index
     const int64_t stride = stats_stride(std::max<int64_t>(1, a->n_rows));
@@ -325,7 +330,12 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtyp
   const int64_t ns = metric_stats_count(md->metric);
   if (ns == 0) return SD_OK;
   SD_TRY(sa_buf.alloc(es * ns * stats_stride(std::max<int64_t>(1, a->n_rows)), st));
-  SD_TRY(metric_stats(a, dtype, md, true, sa_buf.ptr, sa, st));
+  if (defer_a) {  // slot q of the buffer holds statistic q (metric_stats' layout for dot-family metrics)
+    for (int64_t q = 0; q < ns && q < 3; ++q)
+      sa->s[q] = static_cast<char*>(sa_buf.ptr) + size_t(q) * size_t(stats_stride(std::max<int64_t>(1, a->n_rows))) * es;
+  } else {
+    SD_TRY(metric_stats(a, dtype, md, true, sa_buf.ptr, sa, st));
+  }
   if (md->metric == SD_M_KL) return SD_OK;
   sd_index* ix = const_cast<sd_index*>(ix_c);
   if (ix == nullptr) {
@@ -351,7 +361,8 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtyp
 // Fused pairwise distances / kNN over the intersection path.
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
-              void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, cudaStream_t st) {
+              void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, bool a_stats_deferred,
+              cudaStream_t st) {
   const int ck = metric_contrib(md->metric);
   if (ck < 0) { set_error("metric not decomposable over intersections"); return SD_E_UNSUPPORTED; }
   if (ix->dtype != dtype || ix->n_rows != b->n_rows || ix->n_cols != b->n_cols) {
@@ -377,11 +388,24 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
   // computed densely; the sweep skips them
   HybridState hs;
-  if (topk == 0 && ck == C_MUL && ix->n_heavy > 0 && hybrid_enabled() &&
-      (ix->n_tiles >= 4 || hybrid_forced())) {  // small indexes: the sweep is cheap, keep it exact
+  if (isect_hybrid_eligible(ix, md, topk)) {
     if (tm) tm->begin(PH_PASS2);
     SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
     if (tm) tm->end(PH_PASS2);
+  }
+  if (a_stats_deferred) {
+    // the query statistics are only needed by the sweep and the heavy-row
+    // epilogue: on the hybrid path they run on a second side stream,
+    // overlapping the GEMM and the gather
+    cudaStream_t ss = hs.fork ? side_stream(1) : nullptr;
+    if (ss) SD_CUDA_TRY(cudaStreamWaitEvent(ss, hs.fork, 0));
+    Stats tmp;
+    SD_TRY(metric_stats(a, dtype, md, true, const_cast<void*>(sa.s[0]), &tmp, ss ? ss : st));
+    if (ss) {
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.stats_done, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.stats_done, ss));
+      SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.stats_done, 0));
+    }
   }
   const char* be0 = getenv("SD_ISECT_BAND");
   // bytes the sweep streams: postings + their (tile, column) ranges (not the

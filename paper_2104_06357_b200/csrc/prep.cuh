@@ -78,11 +78,15 @@ enum { PH_NORMS = 0, PH_PASS1 = 1, PH_PASS2 = 2, PH_EXPANSION = 3 };
 int metric_semiring(int metric);
 int default_tile(int dtype);
 int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream_t st);
+// defer_a: only lay out the query-side statistics (isect_run computes them)
 int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
-                Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, cudaStream_t st);
+                Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, bool defer_a, cudaStream_t st);
+// could isect_run take the hybrid path (it then computes deferred query statistics)?
+bool isect_hybrid_eligible(const sd_index* ix, const sd_metric_desc* md, int topk);
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
-              void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, cudaStream_t st);
+              void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, bool a_stats_deferred,
+              cudaStream_t st);
 int topk_rows(const void* dist, int64_t m, int64_t n, int64_t ldd, int dtype, int k, int64_t base,
               void* od, int64_t* oi, cudaStream_t st);
 int topk_merge(const void* cd, const int64_t* ci, int64_t m, int lists, int k, int dtype, void* od,
