@@ -639,10 +639,20 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
                                                          const T* __restrict__ dlh, int64_t qpad, int JB) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int64_t qs = qpad + 1;  // padded row stride: lanes read one column across rows
-  T* sv = reinterpret_cast<T*>(smem);
+  // per heavy query (row, statistics), loaded once per CTA ahead of the staged rows
+  int64_t* qrow = reinterpret_cast<int64_t*>(smem);
+  T* qa0 = reinterpret_cast<T*>(qrow + nhq);
+  T* qa1 = qa0 + nhq;
+  T* sv = reinterpret_cast<T*>(smem + ((size_t(nhq) * (8 + 2 * sizeof(T)) + 15) & ~size_t(15)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nblk = (a.n + JB - 1) / JB;
   uint32_t flags = 0;
+  for (int qq = threadIdx.x; qq < nhq; qq += blockDim.x) {
+    const int64_t i = hq[qq];
+    qrow[qq] = i;
+    qa0[qq] = a.sa0 ? a.sa0[i] : T(0);
+    qa1[qq] = a.sa1 ? a.sa1[i] : T(0);
+  }
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int64_t j0 = blk * JB;
     const int jn = int(tmin<int64_t>(JB, a.n - j0));
@@ -666,9 +676,9 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
       gb1[u] = ok && a.sb1 ? a.sb1[j0 + jj] : T(0);
     }
     for (int qq = warp; qq < nhq; qq += int(blockDim.x >> 5)) {
-      const int64_t i = hq[qq];
-      const T ra0 = a.sa0 ? a.sa0[i] : T(0);
-      const T ra1 = a.sa1 ? a.sa1[i] : T(0);
+      const int64_t i = qrow[qq];
+      const T ra0 = qa0[qq];
+      const T ra1 = qa1[qq];
       bool fast_zero;
       T zero_val;
       isect_zero<T, M>(a, ra0, ra1, fast_zero, zero_val);
@@ -698,9 +708,10 @@ int launch_heavy_rows(IsectArgs<T>& a, const int32_t* hq, int nhq, const int32_t
     return SD_E_UNSUPPORTED;
   } else {
     const int64_t per_row = (qpad + 1) * int64_t(sizeof(T));
-    const int JB = int(tmin<int64_t>(64, (smem_optin_bytes() - 4096) / per_row));  // <= 2 cells per lane
+    const int64_t qbytes = (int64_t(nhq) * (8 + 2 * int64_t(sizeof(T))) + 15) & ~int64_t(15);
+    const int JB = int(tmin<int64_t>(64, (smem_optin_bytes() - 4096 - qbytes) / per_row));  // <= 2 cells per lane
     if (JB < 1) { set_error("too many heavy query rows for the hybrid epilogue"); return SD_E_INVALID; }
-    const size_t smem = size_t(JB) * size_t(per_row);
+    const size_t smem = size_t(qbytes) + size_t(JB) * size_t(per_row);
     SD_TRY(prepare_smem(heavy_rows_kernel<T, M>, smem, "heavy_rows_kernel"));
     const int64_t nblk = (a.n + JB - 1) / JB;
     const int blocks = int(tmin<int64_t>(nblk, int64_t(num_sms()) * 8));
