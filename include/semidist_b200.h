@@ -134,8 +134,29 @@ typedef enum {
 
 typedef struct sd_index sd_index; /* opaque J-blocked inverted index of B */
 
+/* Tuning knobs (experiments, tests).  Each knob's default is read ONCE,
+ * when the library loads, from the environment variable named in the
+ * comment; sd_tune overrides it for the rest of the process.  No entry
+ * point reads the environment per call. */
+typedef enum {
+  SD_TUNE_TILE = 0,            /* SD_TILE: index tile rows (fp32; fp64 halves), 0 = default */
+  SD_TUNE_ISECT_PLAN = 1,      /* SD_ISECT_PLAN: 1 = tile-major work items */
+  SD_TUNE_COS_RAW = 2,         /* SD_COS_RAW: 1 = cosine over unscaled postings */
+  SD_TUNE_ISECT_DEBUG = 3,     /* SD_ISECT_DEBUG: 1 skip sweep, 2 skip epilogue (timing only) */
+  SD_TUNE_ISECT_BAND = 4,      /* SD_ISECT_BAND: tiles per L2 band, 0 = automatic */
+  SD_TUNE_ISECT_L2_DIV = 5,    /* SD_ISECT_L2_DIV: band = L2 / div, 0 = automatic */
+  SD_TUNE_HEAVY_DEG = 6,       /* SD_HEAVY_DEG: heavy-row degree threshold, 0 = n_cols/32 */
+  SD_TUNE_HYBRID = 7,          /* SD_HYBRID: 0 off, 1 automatic, 2 forced on small indexes */
+  SD_TUNE_HYBRID_MAX_MB = 8,   /* SD_HYBRID_MAX_MB: largest dense heavy block (MiB) */
+  SD_TUNE_HYBRID_MAX_QUERIES = 9, /* SD_HYBRID_MAX_QUERIES: heavy query rows per call */
+  SD_TUNE_HGEMM = 10,          /* SD_HGEMM: 0 automatic, 1 CUDA-core, 2 mma.sync */
+  SD_TUNE_COUNT = 11
+} sd_tune_knob;
+
 /* ---------------------------------------------------------------- misc */
 SD_API int sd_version(void);
+/* Set knob `knob` to `value`; the old value goes to *previous (nullable). */
+SD_API int sd_tune(int knob, int64_t value, int64_t* previous);
 SD_API const char* sd_last_error(void);
 /* Cumulative number of kernels this library has launched in the process. */
 SD_API uint64_t sd_launch_count(void);

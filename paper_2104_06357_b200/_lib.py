@@ -68,6 +68,7 @@ _CSR = ctypes.POINTER(SdCsr)
 # (name, restype, argtypes) — exactly the declarations of include/semidist_b200.h
 SIGNATURES = [
     ("sd_version", _I, []),
+    ("sd_tune", _I, [_I, _I64, ctypes.POINTER(_I64)]),
     ("sd_last_error", ctypes.c_char_p, []),
     ("sd_launch_count", ctypes.c_uint64, []),
     ("sd_smem_budget", _I, [_I, ctypes.POINTER(_I64)]),
@@ -92,6 +93,11 @@ SIGNATURES = [
     ("sd_topk_merge", _I, [_P, _P, _I64, _I, _I, _I, _P, _P, _P]),
 ]
 
+TUNE_KNOBS = {
+    "tile": 0, "isect_plan": 1, "cos_raw": 2, "isect_debug": 3, "isect_band": 4, "isect_l2_div": 5,
+    "heavy_deg": 6, "hybrid": 7, "hybrid_max_mb": 8, "hybrid_max_queries": 9, "hgemm": 10,
+}
+
 _LIB = None
 
 
@@ -110,6 +116,31 @@ def load():
             fn.argtypes = args
         _LIB = lib
     return _LIB
+
+
+def tune(name, value):
+    """Set a tuning knob (include/semidist_b200.h sd_tune_knob); returns the previous value."""
+    prev = ctypes.c_int64()
+    check(load().sd_tune(TUNE_KNOBS[name], int(value), ctypes.byref(prev)), "sd_tune")
+    return int(prev.value)
+
+
+class tuned:
+    """Context manager: ``with tuned(hybrid=2): ...`` restores the knobs on exit."""
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+        self.saved = {}
+
+    def __enter__(self):
+        for name, value in self.knobs.items():
+            self.saved[name] = tune(name, value)
+        return self
+
+    def __exit__(self, *exc):
+        for name, value in self.saved.items():
+            tune(name, value)
+        return False
 
 
 def last_error():
@@ -132,6 +163,18 @@ def check(status, what=""):
     if status == SD_E_UNSUPPORTED:
         raise NotImplementedError(msg)
     raise RuntimeError(f"libsemidist_b200 status {status}: {msg}")
+
+
+def call(device, name, *args):
+    """Run C entry point ``name`` with ``device`` current (the library takes the
+    SM count, shared-memory limit and side streams from the current device, and
+    a launch into another device's stream fails) and map its status."""
+    import torch
+    fn = getattr(load(), name)
+    if device is None:
+        return check(fn(*args), name)
+    with torch.cuda.device(device):
+        return check(fn(*args), name)
 
 
 def raise_flags(flags, metric_name=""):
@@ -184,8 +227,8 @@ def any_negative(d):
     """True if any stored value of a DeviceCsr is negative (one 4-byte D2H)."""
     flags = new_flags(d.device)
     csr = csr_struct(d)
-    check(load().sd_check_nonnegative(ctypes.byref(csr), dtype_code(d.dtype), flags.data_ptr(),
-                                      stream_handle(d.device)), "sd_check_nonnegative")
+    call(d.device, "sd_check_nonnegative", ctypes.byref(csr), dtype_code(d.dtype), flags.data_ptr(),
+         stream_handle(d.device))
     return bool(int(flags.item()) & SD_FLAG_NEGATIVE)
 
 
@@ -195,13 +238,13 @@ def transform_values(d, transform):
     from .sparse import DeviceCsr
     if transform != "sqrt":
         raise ValueError(f"unknown value transform {transform!r}")
-    lib = load()
     out = torch.empty_like(d.values)
     csr = csr_struct(d)
-    check(lib.sd_sqrt_values(ctypes.byref(csr), dtype_code(d.dtype), out.data_ptr() if d.nnz else None,
-                             stream_handle(d.device)), "sd_sqrt_values")
+    call(d.device, "sd_sqrt_values", ctypes.byref(csr), dtype_code(d.dtype), out.data_ptr() if d.nnz else None,
+         stream_handle(d.device))
     t = DeviceCsr(d.n_rows, d.n_cols, d.indptr, d.indices, out, row_offset=d.row_offset)
     t._host_degrees = d._host_degrees
+    t.transform = transform
     return t
 
 
@@ -212,8 +255,8 @@ class DeviceIndex:
         lib = load()
         handle = ctypes.c_void_p()
         csr = csr_struct(dcsr)
-        check(lib.sd_index_build(ctypes.byref(csr), dtype_code(dcsr.dtype), 0, ctypes.byref(handle),
-                                 stream_handle(dcsr.device)), "sd_index_build")
+        call(dcsr.device, "sd_index_build", ctypes.byref(csr), dtype_code(dcsr.dtype), 0, ctypes.byref(handle),
+             stream_handle(dcsr.device))
         self.handle = handle
         self.n_rows = dcsr.n_rows
         self.bytes = int(lib.sd_index_bytes(handle))
@@ -240,21 +283,19 @@ def device_index(dcsr):
 
 def row_stat(dcsr, kind):
     import torch
-    lib = load()
     out = torch.empty(dcsr.n_rows, dtype=dcsr.dtype, device=dcsr.device)
     csr = csr_struct(dcsr)
-    check(lib.sd_row_stat(ctypes.byref(csr), dtype_code(dcsr.dtype), int(kind), out.data_ptr(),
-                          stream_handle(dcsr.device)), "sd_row_stat")
+    call(dcsr.device, "sd_row_stat", ctypes.byref(csr), dtype_code(dcsr.dtype), int(kind), out.data_ptr(),
+         stream_handle(dcsr.device))
     return out
 
 
 def coo_rows(dcsr):
     import torch
-    lib = load()
     out = torch.empty(dcsr.nnz, dtype=torch.int64, device=dcsr.device)
     csr = csr_struct(dcsr)
-    check(lib.sd_csr_to_coo(ctypes.byref(csr), out.data_ptr() if dcsr.nnz else None,
-                            stream_handle(dcsr.device)), "sd_csr_to_coo")
+    call(dcsr.device, "sd_csr_to_coo", ctypes.byref(csr), out.data_ptr() if dcsr.nnz else None,
+         stream_handle(dcsr.device))
     return out
 
 

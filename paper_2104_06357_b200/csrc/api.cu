@@ -4,6 +4,7 @@
 // kneighbors_detail (knn.py:50-82); every piece of arithmetic runs in the
 // kernels of prep.cu / engine.cu / isect.cu / epilogue.cu / topk.cu.
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -18,6 +19,34 @@ static thread_local std::string g_error;
 void set_error(const std::string& msg) { g_error = msg; }
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Tuning knobs: environment defaults read once (first use), sd_tune afterwards.
+static std::atomic<int64_t> g_knobs[SD_TUNE_COUNT];
+static std::once_flag g_knobs_once;
+
+static void init_knobs() {
+  auto env = [](const char* name, int64_t dflt) -> int64_t {
+    const char* e = getenv(name);
+    return e ? atoll(e) : dflt;
+  };
+  g_knobs[SD_TUNE_TILE] = env("SD_TILE", 0);
+  g_knobs[SD_TUNE_ISECT_PLAN] = env("SD_ISECT_PLAN", 0);
+  g_knobs[SD_TUNE_COS_RAW] = getenv("SD_COS_RAW") ? 1 : 0;
+  g_knobs[SD_TUNE_ISECT_DEBUG] = env("SD_ISECT_DEBUG", 0);
+  g_knobs[SD_TUNE_ISECT_BAND] = env("SD_ISECT_BAND", 0);
+  g_knobs[SD_TUNE_ISECT_L2_DIV] = env("SD_ISECT_L2_DIV", 0);
+  g_knobs[SD_TUNE_HEAVY_DEG] = env("SD_HEAVY_DEG", 0);
+  g_knobs[SD_TUNE_HYBRID] = env("SD_HYBRID", 1);
+  g_knobs[SD_TUNE_HYBRID_MAX_MB] = env("SD_HYBRID_MAX_MB", 1024);
+  g_knobs[SD_TUNE_HYBRID_MAX_QUERIES] = env("SD_HYBRID_MAX_QUERIES", 1024);
+  const char* g = getenv("SD_HGEMM");
+  g_knobs[SD_TUNE_HGEMM] = !g ? 0 : std::string(g) == "simt" ? 1 : std::string(g) == "mma" ? 2 : atoll(g);
+}
+
+int64_t knob(int k) {
+  std::call_once(g_knobs_once, init_knobs);
+  return (k >= 0 && k < SD_TUNE_COUNT) ? g_knobs[k].load(std::memory_order_relaxed) : 0;
+}
 
 // device attributes, cached per device (queried on every launch otherwise)
 static int device_attr(cudaDeviceAttr attr, int fallback) {
@@ -165,6 +194,14 @@ using namespace sd;
 extern "C" {
 
 int sd_version(void) { return SD_ABI_VERSION; }
+
+int sd_tune(int k, int64_t value, int64_t* previous) {
+  if (k < 0 || k >= SD_TUNE_COUNT) { set_error("unknown tuning knob"); return SD_E_INVALID; }
+  const int64_t old = knob(k);
+  g_knobs[k].store(value, std::memory_order_relaxed);
+  if (previous) *previous = old;
+  return SD_OK;
+}
 uint64_t sd_launch_count(void) { return g_launches.load(); }
 const char* sd_last_error(void) { return g_error.c_str(); }
 

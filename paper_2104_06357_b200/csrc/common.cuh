@@ -50,6 +50,9 @@ struct Status {
 
 inline cudaStream_t as_stream(sd_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// tuning knob (sd_tune_knob): environment default read once at load, then sd_tune
+int64_t knob(int k);
+
 int num_sms();
 int64_t smem_optin_bytes();
 int64_t l2_bytes();

@@ -336,7 +336,9 @@ static int run_classes(std::vector<LaunchClass>& classes, const sd_csr* staged, 
 template <typename T>
 static int build_classes(const sd_csr* staged, const std::vector<int64_t>& ptr, const sd_strategy* strat,
                          std::vector<LaunchClass>& classes) {
-  const int64_t optin = smem_optin_bytes();
+  // the pass kernel's own static shared memory (same for every semiring/pass) is not available
+  // to the staging slots: size windows and tables from what is left
+  const int64_t optin = smem_optin_bytes() - static_smem((const void*)pass_kernel<T, SD_SR_DOT, 1>);
   const int64_t n_cols = staged->n_cols;
   const int64_t n = staged->n_rows;
   const int kind = strat ? strat->kind : SD_STRAT_AUTO;

@@ -28,22 +28,14 @@
 
 namespace sd {
 
-namespace {
-
-int64_t env_i64(const char* name, int64_t dflt) {
-  const char* e = getenv(name);
-  return e ? atoll(e) : dflt;
-}
-
-}  // namespace
-
 int64_t hybrid_threshold(int64_t n_cols) {
-  return std::max<int64_t>(64, env_i64("SD_HEAVY_DEG", (n_cols + 31) / 32));
+  const int64_t t = knob(SD_TUNE_HEAVY_DEG);
+  return std::max<int64_t>(64, t > 0 ? t : (n_cols + 31) / 32);
 }
 
-// SD_HYBRID: 0 off, 1 automatic (default), 2 forced even for small indexes (tests)
-bool hybrid_enabled() { return env_i64("SD_HYBRID", 1) != 0; }
-bool hybrid_forced() { return env_i64("SD_HYBRID", 1) == 2; }
+// SD_TUNE_HYBRID: 0 off, 1 automatic (default), 2 forced even for small indexes (tests)
+bool hybrid_enabled() { return knob(SD_TUNE_HYBRID) != 0; }
+bool hybrid_forced() { return knob(SD_TUNE_HYBRID) == 2; }
 
 // ---------------------------------------------------------------- index side
 
@@ -87,7 +79,7 @@ int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st
   const int64_t pad = (nh + 127) / 128 * 128;
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t dense_bytes = b->n_cols * pad * int64_t(es);
-  if (dense_bytes > env_i64("SD_HYBRID_MAX_MB", 1024) << 20) return SD_OK;
+  if (dense_bytes > knob(SD_TUNE_HYBRID_MAX_MB) << 20) return SD_OK;
   Scratch drows;
   SD_TRY(drows.alloc(sizeof(int32_t) * nh, st));
   if (cudaMalloc(&ix->hid, sizeof(int32_t) * b->n_rows) != cudaSuccess || cudaMalloc(&ix->ht, dense_bytes) != cudaSuccess ||
@@ -426,7 +418,7 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
                    cudaStream_t st) {
   hs.nhq = 0;
   const int64_t m = a->n_rows;
-  const int cap = int(env_i64("SD_HYBRID_MAX_QUERIES", 1024));
+  const int cap = int(std::max<int64_t>(1, knob(SD_TUNE_HYBRID_MAX_QUERIES)));
   SD_TRY(hs.qid.alloc(sizeof(int32_t) * std::max<int64_t>(1, m), st));
   SD_TRY(hs.hq.alloc(sizeof(int32_t) * cap, st));
   SD_TRY(hs.count.alloc(sizeof(unsigned int), st));
@@ -450,9 +442,9 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   // fp32: tcgen05 3xTF32 GEMM (M = 128 heavy index rows x N = all heavy
   // queries, hgemm_tc.cu) when they fit one tile (<= 256), else mma.sync
   // 3xTF32 (tile 32 x 128 x 32); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
-  const char* ge = getenv("SD_HGEMM");  // experiment override: "simt", "mma"
-  const bool simt = ge && std::string(ge) == "simt";
-  const bool tc5 = dtype == SD_F32 && ix->ht_tiled && hs.nhq <= 256 && !simt && !(ge && std::string(ge) == "mma");
+  const int64_t ge = knob(SD_TUNE_HGEMM);  // experiment override: 1 CUDA cores, 2 mma.sync
+  const bool simt = ge == 1;
+  const bool tc5 = dtype == SD_F32 && ix->ht_tiled && hs.nhq <= 256 && !simt && ge != 2;
   const bool tc = dtype == SD_F32 && !simt && !tc5;
   const int64_t bm = tc5 ? (hs.nhq + 15) / 16 * 16 : tc ? TG_BM : HG_BM;
   const int64_t bn = tc5 ? 128 : tc ? TG_BN : HG_BN, bkk = tc5 ? tc_kstep() : tc ? TG_BK : HG_BK;

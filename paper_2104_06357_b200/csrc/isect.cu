@@ -35,10 +35,8 @@
 namespace sd {
 
 int default_tile(int dtype) {
-  if (const char* e = getenv("SD_TILE")) {  // experiment override
-    const int t = atoi(e);
-    if (t >= 128 && t <= 65536 && t % 128 == 0) return dtype == SD_F64 ? t / 2 : t;
-  }
+  const int64_t t = knob(SD_TUNE_TILE);  // experiment override
+  if (t >= 128 && t <= 65536 && t % 128 == 0) return int(dtype == SD_F64 ? t / 2 : t);
   return dtype == SD_F64 ? 2048 : 4096;
 }
 
@@ -380,10 +378,9 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // bands of tiles whose postings fit the L2 together, so the index streams
   // from HBM about once while every query sweeps the resident band; bands are
   // split evenly (no short tail band).  SD_ISECT_BAND overrides (tuning).
-  const char* pe = getenv("SD_ISECT_PLAN");  // experiment override: 1 = tile-major items
-  const int tile_major = pe ? atoi(pe) : 0;
+  const int tile_major = int(knob(SD_TUNE_ISECT_PLAN));  // experiment override: 1 = tile-major items
   // cosine over postings pre-divided by the index-row norms (built once per index)
-  const bool cos_scaled = md->metric == SD_M_COSINE && sb.s[1] != nullptr && getenv("SD_COS_RAW") == nullptr;
+  const bool cos_scaled = md->metric == SD_M_COSINE && sb.s[1] != nullptr && knob(SD_TUNE_COS_RAW) == 0;
   if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
   // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
   // computed densely; the sweep skips them
@@ -407,7 +404,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
       SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.stats_done, 0));
     }
   }
-  const char* be0 = getenv("SD_ISECT_BAND");
+  const int64_t be0 = knob(SD_TUNE_ISECT_BAND);
   // bytes the sweep streams: postings + their (tile, column) ranges (not the
   // hybrid block or the other metric's posting copy, which it never touches)
   const int64_t post_bytes = std::max<int64_t>(
@@ -419,15 +416,15 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // Otherwise whole-L2 bands: with heavy rows in the sweep (C2 manhattan 4.9
   // vs 5.9 ms) and for kNN, where every band adds a top-k list per query to
   // merge (C5: 49 vs 56 ms), smaller bands cost more than they save.
-  const char* ld = getenv("SD_ISECT_L2_DIV");
+  const int64_t ld = knob(SD_TUNE_ISECT_L2_DIV);
   // Dense-ish indexes (long posting lists per (tile, column), C4: ~280) also
   // prefer the small bands (C4 46.4 -> 39.6 ms).
   const bool long_lists = ix->nnz > 64 * ix->n_tiles * ix->n_cols;
-  const int64_t div = ld ? atoll(ld) : (topk == 0 && (hs.nhq > 0 || long_lists) ? 5 : 1);
+  const int64_t div = ld > 0 ? ld : (topk == 0 && (hs.nhq > 0 || long_lists) ? 5 : 1);
   const int64_t band_bytes = std::max<int64_t>(1, l2_bytes() / std::max<int64_t>(1, div));
   const int64_t n_bands0 = (post_bytes + band_bytes - 1) / band_bytes;
   const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
-  const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 ? atoll(be0) : auto_band));
+  const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 > 0 ? be0 : auto_band));
   const int64_t max_items = m * band0 * ((ix->n_tiles + band0 - 1) / band0);
   Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
   SD_TRY(order.alloc(sizeof(int32_t) * m, st));
@@ -461,8 +458,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.skip = hs.nhq > 0 ? hs.qid.as<int32_t>() : nullptr;
     args.cos_scaled = cos_scaled ? 1 : 0;
     if (cos_scaled) args.post = static_cast<const Posting<T>*>(ix->post_cos);
-    const char* de = getenv("SD_ISECT_DEBUG");
-    args.debug = de ? atoi(de) : 0;
+    args.debug = int(knob(SD_TUNE_ISECT_DEBUG));
     args.band = band;
     args.strict = md->strict;
     args.k = T(a->n_cols); args.p = T(md->p);

@@ -16,12 +16,14 @@
 
 namespace sd {
 
-// NEGATIVE_RADICAND_TOLERANCE (metrics.py:27).  For a value obtained through a
-// cancelling reformulation or in fp32, the admissible rounding residue also
-// scales with the magnitude of the cancelled terms.
+// NEGATIVE_RADICAND_TOLERANCE (metrics.py:27).  float64 uses the reference's
+// absolute 1e-9 exactly (same error behaviour: a radicand below -1e-9 raises
+// DomainError).  float32 — a precision the reference does not have — also
+// admits the fp32 rounding residue of the cancelled terms, 64·eps·scale
+// (DESIGN.md §5).
 template <typename T>
 __device__ __forceinline__ T clamp_radicand(T x, T scale, uint32_t& flags) {
-  const T tol = fmax(T(1e-9), T(64) * Num<T>::eps() * scale);
+  const T tol = sizeof(T) == 8 ? T(1e-9) : fmax(T(1e-9), T(64) * Num<T>::eps() * scale);
   if (x < -tol) flags |= SD_FLAG_RADICAND;
   return x < T(0) ? T(0) : x;
 }

@@ -92,10 +92,9 @@ def merge_candidates(cand_d, cand_i, k):
     od = torch.empty((m, k), dtype=cand_d.dtype, device=cand_d.device)
     oi = torch.empty((m, k), dtype=torch.int64, device=cand_d.device)
     if m and k:
-        lib = _lib.load()
-        _lib.check(lib.sd_topk_merge(cand_d.contiguous().data_ptr(), cand_i.contiguous().data_ptr(), m, lists,
-                                     int(k), _lib.dtype_code(cand_d.dtype), od.data_ptr(), oi.data_ptr(),
-                                     _lib.stream_handle(cand_d.device)), "sd_topk_merge")
+        cd, ci = cand_d.contiguous(), cand_i.contiguous()
+        _lib.call(cand_d.device, "sd_topk_merge", cd.data_ptr(), ci.data_ptr(), m, lists, int(k),
+                  _lib.dtype_code(cand_d.dtype), od.data_ptr(), oi.data_ptr(), _lib.stream_handle(cand_d.device))
     return od, oi
 
 

@@ -158,9 +158,8 @@ def allocate_output(a, b, semiring, *, dtype=np.float64, device=None):
     from .sparse import _torch_dtype
     out = torch.empty((a.n_rows, b.n_rows), dtype=_torch_dtype(dtype), device=device)
     if out.numel():
-        lib = _lib.load()
-        _lib.check(lib.sd_fill(out.data_ptr(), a.n_rows, b.n_rows, b.n_rows, _lib.dtype_code(out.dtype),
-                               float(semiring.reduce_identity), _lib.stream_handle(out.device)), "sd_fill")
+        _lib.call(out.device, "sd_fill", out.data_ptr(), a.n_rows, b.n_rows, b.n_rows, _lib.dtype_code(out.dtype),
+                  float(semiring.reduce_identity), _lib.stream_handle(out.device))
     return out
 
 
@@ -186,17 +185,16 @@ def _run_pass(a, b, semiring, strategy, out, pass_no):
     da = to_device(a, dtype, device)
     db = to_device(b, dtype, da.device)
     dev_out = torch.from_numpy(np.ascontiguousarray(out)).to(da.device) if host_out else out
-    if not dev_out.is_contiguous():
-        raise ValueError("device output must be contiguous")
+    if dev_out.dim() != 2 or (dev_out.numel() and dev_out.stride(1) != 1):
+        raise ValueError("device output must be a row-major matrix (unit column stride)")
     sid, p = device_id(semiring)
-    lib = _lib.load()
     ca, cb = _lib.csr_struct(da), _lib.csr_struct(db)
     strat = _strategy_struct(strategy)
     rep = _lib.SdReport()
     if dev_out.numel():
-        _lib.check(lib.sd_pass(ctypes.byref(ca), ctypes.byref(cb), _lib.dtype_code(dtype), sid, p, pass_no,
-                               ctypes.byref(strat), dev_out.data_ptr(), b.n_rows, ctypes.byref(rep),
-                               _lib.stream_handle(da.device)), f"pass {pass_no}")
+        _lib.call(da.device, "sd_pass", ctypes.byref(ca), ctypes.byref(cb), _lib.dtype_code(dtype), sid, p, pass_no,
+                  ctypes.byref(strat), dev_out.data_ptr(), dev_out.stride(0), ctypes.byref(rep),
+                  _lib.stream_handle(da.device))
     if host_out:
         out[...] = dev_out.cpu().numpy()
     staged = da if pass_no == 1 else db

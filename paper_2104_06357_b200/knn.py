@@ -58,9 +58,8 @@ def select_topk(row_distances, k, *, device=None):
     od = torch.empty(k, dtype=torch.float64, device=dev)
     oi = torch.empty(k, dtype=torch.int64, device=dev)
     if k:
-        lib = _lib.load()
-        _lib.check(lib.sd_topk_rows(d.data_ptr(), 1, row.size, row.size, _lib.SD_F64, int(k), 0, od.data_ptr(),
-                                    oi.data_ptr(), _lib.stream_handle(dev)), "sd_topk_rows")
+        _lib.call(dev, "sd_topk_rows", d.data_ptr(), 1, row.size, row.size, _lib.SD_F64, int(k), 0, od.data_ptr(),
+                  oi.data_ptr(), _lib.stream_handle(dev))
     return od.cpu().numpy(), oi.cpu().numpy()
 
 
@@ -85,11 +84,10 @@ def knn_device(index, queries, k, spec, *, dtype=np.float32, index_base=0, check
     if k and dq.n_rows:
         md = _lib.metric_struct(name, p, strict, pre_transformed=transform is not None)
         ix = _lib.device_index(di).handle if name != "chebyshev" else None
-        lib = _lib.load()
         cq, cb = _lib.csr_struct(dq), _lib.csr_struct(di)
-        _lib.check(lib.sd_knn(ctypes.byref(cq), ctypes.byref(cb), ix, _lib.dtype_code(tdt), ctypes.byref(md),
-                              int(k), int(index_base), od.data_ptr(), oi.data_ptr(), flags.data_ptr(),
-                              _lib.stream_handle(di.device)), "sd_knn")
+        _lib.call(di.device, "sd_knn", ctypes.byref(cq), ctypes.byref(cb), ix, _lib.dtype_code(tdt), ctypes.byref(md),
+                  int(k), int(index_base), od.data_ptr(), oi.data_ptr(), flags.data_ptr(),
+                  _lib.stream_handle(di.device))
     if check_flags:
         _lib.raise_flags(int(flags.item()), name)
     return od, oi, flags
@@ -141,10 +139,8 @@ def kneighbors_detail(index, queries, k, spec, strategy=None, batch_rows=None, w
         bd = torch.empty((stop - start, k), dtype=tdt, device=d.device)
         bi = torch.empty((stop - start, k), dtype=torch.int64, device=d.device)
         if k and d.numel():
-            lib = _lib.load()
-            _lib.check(lib.sd_topk_rows(d.data_ptr(), stop - start, index.n_rows, index.n_rows,
-                                        _lib.dtype_code(tdt), int(k), 0, bd.data_ptr(), bi.data_ptr(),
-                                        _lib.stream_handle(d.device)), "sd_topk_rows")
+            _lib.call(d.device, "sd_topk_rows", d.data_ptr(), stop - start, index.n_rows, d.stride(0),
+                      _lib.dtype_code(tdt), int(k), 0, bd.data_ptr(), bi.data_ptr(), _lib.stream_handle(d.device))
         dists[start:stop] = _lib.as_numpy_f64(bd)
         ids[start:stop] = bi.cpu().numpy()
         timings["topk"] += time.perf_counter() - t0

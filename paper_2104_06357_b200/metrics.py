@@ -183,11 +183,10 @@ def expansion_apply(dots, norms_a, norms_b, spec, *, n_cols, sums_a=None, sums_b
     pa, pb = arrays(sa), arrays(sb)
     flags = _lib.new_flags(dev)
     md = _lib.metric_struct(name, p, strict)
-    lib = _lib.load()
     if d.numel():
         m, n = d.shape
-        _lib.check(lib.sd_expand(d.data_ptr(), m, n, n, _lib.dtype_code(tdt), ctypes.byref(md), int(n_cols),
-                                 pa, pb, flags.data_ptr(), _lib.stream_handle(dev)), "sd_expand")
+        _lib.call(dev, "sd_expand", d.data_ptr(), m, n, n, _lib.dtype_code(tdt), ctypes.byref(md), int(n_cols),
+                  pa, pb, flags.data_ptr(), _lib.stream_handle(dev))
     _lib.raise_flags(int(flags.item()), name)
     return _lib.as_numpy_f64(d)
 
@@ -232,7 +231,6 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
     flags = _lib.new_flags(da.device)
     md = _lib.metric_struct(name, p, strict, pre_transformed=transform is not None)
     phases = (ctypes.c_float * 4)()
-    lib = _lib.load()
     ca, cb = _lib.csr_struct(da), _lib.csr_struct(db)
     if fused:
         strat = _lib.strategy_struct(_lib.STRAT_AUTO)
@@ -241,10 +239,9 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
         strat = _strategy_struct(resolve_strategy(strategy, a, b))
         index = None
     rep = _lib.SdReport()
-    _lib.check(lib.sd_pairwise(ctypes.byref(ca), ctypes.byref(cb), index, _lib.dtype_code(tdt), ctypes.byref(md),
-                               ctypes.byref(strat), out_buf.data_ptr() if out.numel() else None, ldo,
-                               flags.data_ptr(), ctypes.byref(rep), phases, _lib.stream_handle(da.device)),
-               "sd_pairwise")
+    _lib.call(da.device, "sd_pairwise", ctypes.byref(ca), ctypes.byref(cb), index, _lib.dtype_code(tdt),
+              ctypes.byref(md), ctypes.byref(strat), out_buf.data_ptr() if out.numel() else None, ldo,
+              flags.data_ptr(), ctypes.byref(rep), phases, _lib.stream_handle(da.device))
     if check_flags:
         _lib.raise_flags(int(flags.item()), name)
     timings = {"norms": phases[0] / 1e3, "pass1": phases[1] / 1e3, "pass2": phases[2] / 1e3,

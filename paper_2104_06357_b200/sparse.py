@@ -246,6 +246,7 @@ class DeviceCsr:
             raise ValueError("DeviceCsr values must be float32 or float64")
         self.cache = {}
         self._host_degrees = None
+        self.transform = None   # value transform these values already carry ("sqrt" for hellinger)
 
     @property
     def device(self):
@@ -277,6 +278,7 @@ class DeviceCsr:
                         row_offset=self.row_offset + start)
         if self._host_degrees is not None:
             sub._host_degrees = self._host_degrees[start:stop]
+        sub.transform = self.transform
         return sub
 
 
@@ -291,7 +293,27 @@ def to_device(m, dtype="float64", device=None, transform=None):
     ("sqrt" for Hellinger, metrics.py:205-207)."""
     import torch
     if isinstance(m, DeviceCsr):
-        return m
+        tdtype = _torch_dtype(dtype)
+        if m.dtype != tdtype:   # compute dtype differs from the stored one: a converted copy, cached
+            key = ("dtype", tdtype)
+            conv = m.cache.get(key)
+            if conv is None:
+                conv = DeviceCsr(m.n_rows, m.n_cols, m.indptr, m.indices, m.values.to(tdtype),
+                                 row_offset=m.row_offset)
+                conv._host_degrees = m._host_degrees
+                conv.transform = m.transform
+                m.cache[key] = conv
+            m = conv
+        if transform is None or m.transform == transform:
+            return m
+        if m.transform is not None:
+            raise ValueError(f"matrix already carries value transform {m.transform!r}")
+        key = ("transform", transform)
+        hit = m.cache.get(key)
+        if hit is None:
+            hit = _transformed(m, transform)
+            m.cache[key] = hit
+        return hit
     tdtype = _torch_dtype(dtype)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     key = (tdtype, str(dev), transform)
@@ -314,13 +336,19 @@ def to_device(m, dtype="float64", device=None, transform=None):
     )
     d._host_degrees = np.diff(indptr)
     if transform is not None:
-        from . import _lib
-        from .errors import DomainError
-        if _lib.any_negative(d):   # domain check on the raw values (metrics.py:308-311)
-            raise DomainError("hellinger requires non-negative inputs")
-        d = _lib.transform_values(d, transform)
+        d = _transformed(d, transform)
     per[key] = d
     return d
+
+
+def _transformed(d, transform):
+    """Value transform of a DeviceCsr on device, after the domain check on the
+    raw values (metrics.py:308-311, 332-338)."""
+    from . import _lib
+    from .errors import DomainError
+    if _lib.any_negative(d):
+        raise DomainError("hellinger requires non-negative inputs")
+    return _lib.transform_values(d, transform)
 
 
 def _torch_dtype(dtype):

@@ -345,18 +345,19 @@ def test_fused_chebyshev_matches_engine_and_oracle(dtype):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_tile_bands_partial_and_invariant(dtype, monkeypatch):
-    """Multi-tile index swept in bands of tiles (SD_ISECT_BAND): a last, partial
+def test_tile_bands_partial_and_invariant(dtype):
+    """Multi-tile index swept in bands of tiles (knob isect_band): a last, partial
     band (empty tile ranges for some items) and every band size give bitwise
     the same distances and neighbours, matching the oracle on a sample."""
     idx = _f32(sd.generate(sd.GenSpec(9500, 3000, "zipf", zipf_s=1.4, zipf_max_degree=900, seed=51)))
     q = _f32(sd.generate(sd.GenSpec(150, 3000, "zipf", zipf_s=1.4, zipf_max_degree=900, seed=52)))
     spec = sd.metric_registry("cosine")
     outs, knns = [], []
-    for band in ("1", "2", "3", "1000"):
-        monkeypatch.setenv("SD_ISECT_BAND", band)
-        outs.append(sd.pairwise_distances(q, idx, spec, dtype=dtype))
-        knns.append(sd.kneighbors(idx, q, 9, spec, dtype=dtype))
+    from paper_2104_06357_b200 import _lib
+    for band in (1, 2, 3, 1000):
+        with _lib.tuned(isect_band=band):
+            outs.append(sd.pairwise_distances(q, idx, spec, dtype=dtype))
+            knns.append(sd.kneighbors(idx, q, 9, spec, dtype=dtype))
     for o, r in zip(outs[1:], knns[1:]):
         np.testing.assert_array_equal(o, outs[0])
         np.testing.assert_array_equal(r.indices, knns[0].indices)
@@ -371,11 +372,11 @@ DOT_FAMILY = ("cosine", "euclidean", "correlation", "dot", "dice", "jaccard", "h
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_hybrid_heavy_rows_vs_oracle(dtype, monkeypatch):
+def test_hybrid_heavy_rows_vs_oracle(dtype):
     """Hybrid path (hybrid.cu): query rows with >= max(64, n_cols/32) nonzeros are
     computed densely (GEMM against the index's heavy rows + gather over its
     light rows) and the sweep skips them.  Every dot-family metric against the
-    oracle, and against the sweep-only path (SD_HYBRID=0) within rounding."""
+    oracle, and against the sweep-only path (knob hybrid=0) within rounding."""
     import torch
     from paper_2104_06357_b200 import _lib
     idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
@@ -384,34 +385,34 @@ def test_hybrid_heavy_rows_vs_oracle(dtype, monkeypatch):
     assert len(heavy) >= 64
     rows = np.sort(np.concatenate([heavy[:40], np.arange(0, idx.n_rows, 37)]))
     q = _gather_rows(idx, np.unique(rows))
-    monkeypatch.setenv("SD_HYBRID", "2")
-    assert _lib.device_index(sd.to_device(_host(idx), dtype)).heavy_rows == len(heavy)
-    for name in DOT_FAMILY:
-        a, b = (q, idx) if name not in ("dice", "jaccard", "russelrao") else (q.with_values(np.ones(q.nnz)),
-                                                                              idx.with_values(np.ones(idx.nnz)))
-        a, b = _host(a), _host(b)
-        spec = sd.metric_registry(name)
-        got = sd.pairwise_distances(a, b, spec, dtype=dtype)
-        ref = O.pairwise_distances(a, b, name)
-        assert_parity(got, ref, a, b, name, dtype, what=f"hybrid/{name}")
-        monkeypatch.setenv("SD_HYBRID", "0")
-        sweep = sd.pairwise_distances(_host(a), _host(b), spec, dtype=dtype)
-        monkeypatch.setenv("SD_HYBRID", "2")
-        assert_parity(got, sweep, a, b, name, dtype, what=f"hybrid vs sweep/{name}")
+    with _lib.tuned(hybrid=2):
+        assert _lib.device_index(sd.to_device(_host(idx), dtype)).heavy_rows == len(heavy)
+        for name in DOT_FAMILY:
+            a, b = (q, idx) if name not in ("dice", "jaccard", "russelrao") else (
+                q.with_values(np.ones(q.nnz)), idx.with_values(np.ones(idx.nnz)))
+            a, b = _host(a), _host(b)
+            spec = sd.metric_registry(name)
+            got = sd.pairwise_distances(a, b, spec, dtype=dtype)
+            ref = O.pairwise_distances(a, b, name)
+            assert_parity(got, ref, a, b, name, dtype, what=f"hybrid/{name}")
+            with _lib.tuned(hybrid=0):
+                sweep = sd.pairwise_distances(_host(a), _host(b), spec, dtype=dtype)
+            assert_parity(got, sweep, a, b, name, dtype, what=f"hybrid vs sweep/{name}")
     torch.cuda.synchronize()
 
 
 @pytest.mark.parametrize("n_heavy_q", [17, 300])
-def test_hybrid_gemm_routes(n_heavy_q, monkeypatch):
+def test_hybrid_gemm_routes(n_heavy_q):
     """The heavy block's GEMM: tcgen05 (<= 256 heavy queries, N = 32 here) and
     the mma.sync fallback (> 256), both against the oracle (fp32)."""
     idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
     deg = np.diff(np.asarray(idx.indptr))
     heavy = np.flatnonzero(deg >= max(64, -(-idx.n_cols // 32)))
     q = _gather_rows(idx, np.sort(heavy[:n_heavy_q]))
-    monkeypatch.setenv("SD_HYBRID", "2")
+    from paper_2104_06357_b200 import _lib
     for name in ("cosine", "euclidean"):
         a, b = _host(q), _host(idx)
-        got = sd.pairwise_distances(a, b, sd.metric_registry(name), dtype=np.float32)
+        with _lib.tuned(hybrid=2):
+            got = sd.pairwise_distances(a, b, sd.metric_registry(name), dtype=np.float32)
         ref = O.pairwise_distances(a, b, name)
         assert_parity(got, ref, a, b, name, np.float32, what=f"hybrid gemm {n_heavy_q}/{name}")

@@ -119,3 +119,23 @@ def test_reference_semiring_objects_resolve(reference_semidist):
     assert device_id(ref.tropical_min_plus())[0] == 1
     with pytest.raises(NotImplementedError):
         device_id(ref.Semiring("custom", np.add, 0.0, np.add, 0.0, False))
+
+
+def test_parity_rule_is_tight():
+    """tests/parity.py accepts the oracle against itself and rejects a relative
+    perturbation of 20x the BASELINE rtol on every metric (the rule has no
+    sqrt(rtol)- or n_cols-sized floors any more)."""
+    from oracle import semidist_oracle as O
+    from parity import check_cells
+    A = O.Csr.of(sd.generate(sd.GenSpec(30, 400, "zipf", zipf_s=1.3, zipf_max_degree=120, seed=3)))
+    B = O.Csr.of(sd.generate(sd.GenSpec(50, 400, "zipf", zipf_s=1.3, zipf_max_degree=120, seed=4)))
+    for name in O.METRIC_NAMES:
+        p = 1.5 if name == "minkowski" else None
+        ref = O.pairwise_distances_c(A, B, name, p=p, strict=False, threads=2)
+        ref = np.where(ref >= 1e308, 0.0, ref)
+        for dt, rtol in ((np.float64, 1e-12), (np.float32, 1e-5)):
+            assert check_cells(ref, ref, A, B, name, dt, p).all(), name
+            big = np.abs(ref) > 1e-3
+            bumped = ref * (1 + 20 * rtol) + 20 * rtol * np.sign(ref)
+            ok = check_cells(bumped, ref, A, B, name, dt, p)
+            assert ok[big].mean() < 0.1, (name, dt, ok[big].mean())

@@ -108,3 +108,55 @@ def test_oracle_vs_live_reference(reference_semidist):
         want = sd.pairwise_distances(A, B, sd.metric_registry(name))
         got = O.pairwise_distances(A, B, name)
         np.testing.assert_array_equal(got, want)
+
+
+def test_c_oracle_pinned_to_golden(golden):
+    """The C restatement (oracle/semidist_oracle.c, used for config-scale parity)
+    equals every golden pairwise case to rounding — sequential instead of
+    numpy's pairwise summation — and bit-for-bit where the sums are exact."""
+    cases, arrays = golden
+    n = 0
+    for c in cases:
+        if c["kind"] != "pairwise" or c["strategy"] not in (None, "auto"):
+            continue
+        a, b = csr(arrays, c["a"]), csr(arrays, c["b"])
+        ref = arrays[c["id"] + ".out"]
+        got = O.pairwise_distances_c(a, b, c["metric"], p=c["p"], strict=c["strict"], threads=4)
+        sat = ref >= 1e308
+        assert ((got >= 1e308) == sat).all(), c["id"]
+        if c["metric"] in ("chebyshev", "hamming", "jaccard", "dice", "russelrao"):
+            np.testing.assert_array_equal(got, ref, err_msg=c["id"])
+        else:
+            np.testing.assert_allclose(np.where(sat, 0, got), np.where(sat, 0, ref), rtol=1e-14, atol=1e-14,
+                                       err_msg=c["id"])
+        n += 1
+    assert n >= 15
+
+
+def test_c_oracle_vs_numpy_port_midsize():
+    """C restatement vs the bitwise-pinned numpy port on a 40 x 3000 power-law case."""
+    A = O.Csr.of(_zipf(40, 3000, 1.3, 700, 5))
+    B = O.Csr.of(_zipf(300, 3000, 1.3, 700, 6))
+    for name in O.METRIC_NAMES:
+        p = 1.5 if name == "minkowski" else None
+        want = O.pairwise_distances(A, B, name, p=p, strict=False)
+        got = O.pairwise_distances_c(A, B, name, p=p, strict=False, threads=3)
+        sat = want >= 1e308
+        assert ((got >= 1e308) == sat).all(), name
+        np.testing.assert_allclose(np.where(sat, 0, got), np.where(sat, 0, want), rtol=1e-12, atol=1e-12,
+                                   err_msg=name)
+
+
+def test_c_oracle_domain_errors():
+    a = O.csr_of_dense([[0.5, 0.5]])
+    b = O.csr_of_dense([[1.0, 0.0]])
+    with pytest.raises(O.OracleDomainError):
+        O.pairwise_distances_c(a, b, "kl")
+    assert O.pairwise_distances_c(a, b, "kl", strict=False)[0, 0] == 1e308
+    with pytest.raises(O.OracleDomainError):
+        O.pairwise_distances_c(O.csr_of_dense([[-1.0, 0.5]]), b, "hellinger")
+
+
+def _zipf(n, k, s, mx, seed):
+    import paper_2104_06357_b200 as sd
+    return sd.generate(sd.GenSpec(n, k, "zipf", zipf_s=s, zipf_max_degree=mx, seed=seed))
