@@ -16,7 +16,9 @@ sqrt(rtol) or rtol * n_cols any more:
     cosine                         : G_ij / (||a|| ||b||) + |1 - d| (the norms' own rounding)
     correlation                    : (k G_ij + |s_a s_b|) / den + |1 - d| * (cond. of den)
     dice / jaccard / russelrao     : derivative of the expansion w.r.t. the dot times G_ij
-    kl                             : sum over A_i ∩ B_j of |a log(a/b)|
+    kl                             : sum over A_i ∩ B_j of |a log(a/b)|, plus (u_T/rtol) * sum of a
+                                     over A_i ∩ B_j: log(a/b) of a rounded quotient is off by ~u_T
+                                     absolutely, however small the term (a ~ b)
     chebyshev                      : 0 (float64 bit-exact; float32 relative rtol only)
 
 G and the KL magnitude are computed exactly by the C oracle's magnitude mode
@@ -77,7 +79,7 @@ def abs_dot(a, b):
     return pairwise_distances_c(a, b, "dot", magnitude=True)
 
 
-def magnitude(a, b, metric, ref, p=None):
+def magnitude(a, b, metric, ref, dtype, p=None):
     """M_ij of the value test (None for metrics compared on the radicand)."""
     a, b = Csr.of(a), Csr.of(b)
     k = float(a.n_cols)
@@ -85,7 +87,10 @@ def magnitude(a, b, metric, ref, p=None):
         s = _sum(one_sided(a, metric), one_sided(b, metric))
         return s / max(1.0, k) if metric == "hamming" else s
     if metric == "kl":
-        return pairwise_distances_c(a, b, "kl", magnitude=True)
+        u = UNIT_ROUNDOFF[np.dtype(dtype)] / RTOL[np.dtype(dtype)]
+        mass = pairwise_distances_c(a, Csr(b.n_rows, b.n_cols, b.indptr, b.indices, np.ones_like(b.values)), "dot",
+                                    magnitude=True)
+        return pairwise_distances_c(a, b, "kl", magnitude=True) + u * mass
     if metric == "chebyshev":
         return np.zeros((a.n_rows, b.n_rows))
     na, nb = _norm(a, "l2"), _norm(b, "l2")
@@ -161,7 +166,7 @@ def check_cells(got, ref, a, b, metric, dtype, p=None):
         # the output itself is rounded to dtype: that much value error is always admissible
         floor = u * (1.0 + np.abs(ref)) if metric == "hellinger" else u * np.abs(ref)
         return ok | (err <= rtol * np.abs(ref) + floor)
-    atol = C_SLACK * rtol * magnitude(a, b, metric, ref, p)
+    atol = C_SLACK * rtol * magnitude(a, b, metric, ref, dtype, p)
     if metric in ONE_MINUS:
         atol = atol + u * (1.0 + np.abs(ref))
     return err <= rtol * np.abs(ref) + atol
