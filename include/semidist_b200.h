@@ -119,7 +119,8 @@ typedef struct {
   double p;                /* minkowski order */
   int32_t pre_transformed; /* 1: a, b (and index) already carry the metric's value
                               transform (sqrt for hellinger, metrics.py:332-338) */
-  int32_t reserved;
+  int32_t stages;          /* sd_expand only: 0 expansion + post-scale, 1 expansion only
+                              (MetricSpec.expansion), 2 post-scale only (MetricSpec.post_scale) */
 } sd_metric_desc;
 
 /* Row statistic kinds for sd_row_stat (sparse.py:257-273). */
@@ -245,6 +246,68 @@ SD_API int sd_topk_rows(const void* dist, int64_t m, int64_t n, int64_t ldd, int
  * global top-k with the same (distance, index) order. */
 SD_API int sd_topk_merge(const void* cand_dist, const int64_t* cand_idx, int64_t m, int lists,
                   int k, int dtype, void* out_dist, int64_t* out_idx, sd_stream_t stream);
+
+/* ------------------------------------------- drop-in utilities (device) */
+/* numpy ufuncs segment_reduce supports (sparse.py:31-53). */
+typedef enum {
+  SD_UFUNC_ADD = 0, SD_UFUNC_MAXIMUM = 1, SD_UFUNC_MINIMUM = 2, SD_UFUNC_MULTIPLY = 3
+} sd_ufunc;
+/* out[s] = ufunc.reduce(values[bounds[s]:bounds[s+1]]), identity for empty
+ * segments (segment_reduce, sparse.py:31-53), with numpy's association:
+ * add.reduceat is v[0] + pairwise_sum(v[1:]), so results are BITWISE those
+ * of the reference.  The caller has checked that bounds tile the values. */
+SD_API int sd_segment_reduce(const void* values, int64_t n_values, const int64_t* bounds,
+                      int64_t n_segments, int dtype, int ufunc, double identity, void* out,
+                      sd_stream_t stream);
+/* mix32 of the low 32 bits of each key (hashtable.py:21-29). */
+SD_API int sd_mix32(const int64_t* keys, int64_t n, uint64_t* out, sd_stream_t stream);
+/* HashAccumulator.build (hashtable.py:43-63): table_keys/values[capacity],
+ * empty slots hold INT64_MAX (EMPTY_SLOT, hashtable.py:12); n < capacity. */
+SD_API int sd_hash_build(const int64_t* keys, const double* values, int64_t n, int64_t capacity,
+                  int64_t* table_keys, double* table_values, sd_stream_t stream);
+/* HashAccumulator.probe_many (hashtable.py:80-106). */
+SD_API int sd_hash_probe(const int64_t* table_keys, const double* table_values, int64_t capacity,
+                  const int64_t* queries, int64_t n, double* out_values, uint8_t* out_found,
+                  sd_stream_t stream);
+/* out[i] = ⊗(x[i], y[i]) of a semiring (Semiring.product_op, semiring.py:36-119). */
+SD_API int sd_semiring_apply(int semiring, double p, const double* x, const double* y, int64_t n,
+                      double* out, sd_stream_t stream);
+/* Dense brute-force arbiter (oracle.py:35-190): out[i*n+j] = the textbook
+ * formula of `metric` over all k columns of dense rows da[i], db[j]; the
+ * engine-independent check behind `verify` (verification.py:54-71). */
+SD_API int sd_dense_pairwise(const double* da, const double* db, int64_t m, int64_t n, int64_t k,
+                      const sd_metric_desc* metric, double* out, uint32_t* dev_flags,
+                      sd_stream_t stream);
+
+/* Why sd_canonicalize rejected its input (sparse.py:135-170 error order). */
+typedef enum {
+  SD_INVALID_NONE = 0,
+  SD_INVALID_NEGATIVE_OFFSET = 1, /* NegativeOffset(row, offset=value)        */
+  SD_INVALID_INDPTR_START = 2,    /* NonMonotonicIndptr(0): indptr[0] = value  */
+  SD_INVALID_DECREASING = 3,      /* NonMonotonicIndptr(row)                   */
+  SD_INVALID_NNZ = 4,             /* ValueError: indptr[-1] = value != nnz      */
+  SD_INVALID_COLUMN = 5           /* IndexOutOfBounds(row, column, n_cols=value) */
+} sd_invalid_kind;
+
+typedef struct {
+  int32_t kind; /* sd_invalid_kind */
+  int32_t pad;
+  int64_t row;
+  int64_t column;
+  int64_t value;
+} sd_invalid;
+
+/* validate_and_canonicalize (sparse.py:135-202) on device: validates a raw
+ * CSR triple (int64 indptr/indices, float64 values) in the reference's error
+ * order (status SD_E_INVALID, details in *why), then sorts each row's
+ * columns (stable), sums duplicates in input order with numpy's reduceat
+ * association (bitwise the reference's values), drops the zeros and writes
+ * the canonical CSR into out_* (capacity nnz entries; out_indptr n_rows+1).
+ * *out_nnz (host) receives the canonical entry count; synchronises `stream`. */
+SD_API int sd_canonicalize(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* indptr,
+                    const int64_t* indices, const double* values, int64_t* out_indptr,
+                    int64_t* out_indices, double* out_values, int64_t* out_nnz, sd_invalid* why,
+                    sd_stream_t stream);
 
 #ifdef __cplusplus
 }

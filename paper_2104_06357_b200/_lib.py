@@ -56,7 +56,12 @@ class SdReport(ctypes.Structure):
 
 class SdMetricDesc(ctypes.Structure):
     _fields_ = [("metric", ctypes.c_int32), ("strict", ctypes.c_int32), ("p", ctypes.c_double),
-                ("pre_transformed", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("pre_transformed", ctypes.c_int32), ("stages", ctypes.c_int32)]
+
+
+class SdInvalid(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32), ("row", ctypes.c_int64),
+                ("column", ctypes.c_int64), ("value", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p
@@ -91,6 +96,14 @@ SIGNATURES = [
     ("sd_knn", _I, [_CSR, _CSR, _P, _I, ctypes.POINTER(SdMetricDesc), _I, _I64, _P, _P, _P, _P]),
     ("sd_topk_rows", _I, [_P, _I64, _I64, _I64, _I, _I, _I64, _P, _P, _P]),
     ("sd_topk_merge", _I, [_P, _P, _I64, _I, _I, _I, _P, _P, _P]),
+    ("sd_segment_reduce", _I, [_P, _I64, _P, _I64, _I, _I, _D, _P, _P]),
+    ("sd_mix32", _I, [_P, _I64, _P, _P]),
+    ("sd_hash_build", _I, [_P, _P, _I64, _I64, _P, _P, _P]),
+    ("sd_hash_probe", _I, [_P, _P, _I64, _P, _I64, _P, _P, _P]),
+    ("sd_semiring_apply", _I, [_I, _D, _P, _P, _I64, _P, _P]),
+    ("sd_dense_pairwise", _I, [_P, _P, _I64, _I64, _I64, ctypes.POINTER(SdMetricDesc), _P, _P, _P]),
+    ("sd_canonicalize", _I, [_I64, _I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
+                             ctypes.POINTER(SdInvalid), _P]),
 ]
 
 TUNE_KNOBS = {
@@ -213,9 +226,9 @@ def strategy_struct(kind, capacity=0, load=0.5):
     return SdStrategy(int(kind), int(capacity), float(load))
 
 
-def metric_struct(name, p=None, strict=True, pre_transformed=False):
+def metric_struct(name, p=None, strict=True, pre_transformed=False, stages=0):
     return SdMetricDesc(METRIC_IDS[name], 1 if strict else 0, float(p) if p is not None else 0.0,
-                        1 if pre_transformed else 0, 0)
+                        1 if pre_transformed else 0, int(stages))
 
 
 def new_flags(device):

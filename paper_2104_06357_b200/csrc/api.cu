@@ -152,7 +152,9 @@ static int engine_pairwise(const sd_csr* a, const sd_csr* b, int dtype, const sd
   }
   if (md->metric == SD_M_KL && miss.ptr == nullptr) return SD_OK;
   tm.begin(PH_EXPANSION);
-  SD_TRY(expand(out, a->n_rows, b->n_rows, ldo, dtype, md, a->n_cols, sa, sb, miss.ptr, flags, st));
+  sd_metric_desc full = *md;  // the distance path always applies expansion and post-scale
+  full.stages = 0;
+  SD_TRY(expand(out, a->n_rows, b->n_rows, ldo, dtype, &full, a->n_cols, sa, sb, miss.ptr, flags, st));
   tm.end(PH_EXPANSION);
   return SD_OK;
 }
@@ -286,9 +288,10 @@ int sd_pairwise(const sd_csr* a, const sd_csr* b, const sd_index* index, int dty
 int sd_expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd_metric_desc* md, int64_t n_cols,
               const void* const* stats_a, const void* const* stats_b, uint32_t* dev_flags, sd_stream_t stream) {
   SD_TRY(check_metric(md));
+  if (md->stages < 0 || md->stages > 2) { set_error("stages must be 0, 1 or 2"); return SD_E_INVALID; }
   Stats sa, sb;
   const int64_t ns = metric_expand_stats_count(md->metric);
-  if (!is_namm(md->metric) && md->metric != SD_M_KL) {
+  if (!is_namm(md->metric) && md->metric != SD_M_KL && md->stages != 2) {
     for (int64_t q = 0; q < ns; ++q) {
       sa.s[q] = stats_a ? stats_a[q] : nullptr;
       sb.s[q] = stats_b ? stats_b[q] : nullptr;

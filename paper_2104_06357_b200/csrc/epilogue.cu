@@ -79,7 +79,7 @@ template <typename T>
 __global__ void expand_kernel(T* __restrict__ d, int64_t m, int64_t n, int64_t ldo, int metric,
                               const T* __restrict__ a0, const T* __restrict__ a1,
                               const T* __restrict__ b0, const T* __restrict__ b1,
-                              const T* __restrict__ miss, int strict, T k, T p, uint32_t* flags) {
+                              const T* __restrict__ miss, int strict, int stage, T k, T p, uint32_t* flags) {
   uint32_t f = 0;
   const int64_t total = m * n;
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
@@ -93,8 +93,8 @@ __global__ void expand_kernel(T* __restrict__ d, int64_t m, int64_t n, int64_t l
         continue;
       }
     }
-    *cell = expand_cell<T>(metric, *cell, a0 ? a0[i] : T(0), a1 ? a1[i] : T(0), b0 ? b0[j] : T(0),
-                           b1 ? b1[j] : T(0), k, p, f);
+    *cell = expand_stage<T>(metric, stage, *cell, a0 ? a0[i] : T(0), a1 ? a1[i] : T(0), b0 ? b0[j] : T(0),
+                            b1 ? b1[j] : T(0), k, p, f);
   }
   f = __reduce_or_sync(0xffffffffu, f);
   if (f && lane_id() == 0) atomicOr(flags, f);
@@ -109,7 +109,7 @@ int expand(void* dots, int64_t m, int64_t n, int64_t ldo, int dtype, const sd_me
     expand_kernel<T><<<blocks, 256, 0, st>>>(
         static_cast<T*>(dots), m, n, ldo, md->metric, static_cast<const T*>(sa.s[0]),
         static_cast<const T*>(sa.s[1]), static_cast<const T*>(sb.s[0]), static_cast<const T*>(sb.s[1]),
-        static_cast<const T*>(miss), md->strict, T(n_cols), T(md->p), flags);
+        static_cast<const T*>(miss), md->strict, md->stages, T(n_cols), T(md->p), flags);
     SD_LAUNCH_CHECK();
     return SD_OK;
   });

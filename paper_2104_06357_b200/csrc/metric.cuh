@@ -99,6 +99,26 @@ __device__ __forceinline__ T expand_cell(int metric, T d, T a0, T a1, T b0, T b1
   }
 }
 
+// One stage of the epilogue (sd_metric_desc.stages): 0 both, 1 the expansion
+// alone (MetricSpec.expansion), 2 the post-scale alone (MetricSpec.post_scale).
+// Euclidean is the only metric with both (metrics.py:200-202); every other
+// metric has one of them, which expand_cell applies in full.
+template <typename T>
+__device__ __forceinline__ T expand_stage(int metric, int stage, T d, T a0, T a1, T b0, T b1, T k, T p,
+                                          uint32_t& flags) {
+  const bool has_post = metric == SD_M_EUCLIDEAN || metric == SD_M_HAMMING || metric == SD_M_JENSENSHANNON ||
+                        metric == SD_M_MINKOWSKI;
+  const bool has_exp = metric <= SD_M_RUSSELRAO;  // the dot family, kl (identity)
+  if (stage == 1) {
+    if (!has_exp) return d;
+    if (metric == SD_M_EUCLIDEAN) return clamp_radicand(add_rn(sub_rn(a0, mul_rn(T(2), d)), b0), add_rn(a0, b0), flags);
+  } else if (stage == 2) {
+    if (!has_post) return d;
+    if (metric == SD_M_EUCLIDEAN) return sqrt_rn(d);
+  }
+  return expand_cell<T>(metric, d, a0, a1, b0, b1, k, p, flags);
+}
+
 // ---- contributions of one intersecting column for the fused path
 enum ContribKind { C_MUL = 0, C_KL = 1, C_ABS = 2, C_ABSPOW = 3, C_CANBERRA = 4, C_MISMATCH = 5, C_JS = 6,
                    C_MAX = 7 /* chebyshev: running max over intersections + top-K hit masks */ };

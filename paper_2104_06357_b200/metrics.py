@@ -37,16 +37,25 @@ BINARY_PREFERRED = frozenset({"dice", "jaccard", "russelrao", "hamming"})
 
 
 class _Epilogue:
-    """Marker for a catalog row's expansion / post-scale stage.  The stage
-    itself is device code (csrc/metric.cuh ``expand_cell``), applied inside
-    ``sd_pairwise`` or through ``expansion_apply``."""
+    """One catalog row's expansion (``(dots, stats_a, stats_b, k) -> matrix``)
+    or post-scale (``(matrix, k) -> matrix``) stage, evaluated on device by
+    sd_expand (csrc/metric.cuh ``expand_stage``) — the same per-cell code the
+    fused kernels apply inside ``sd_pairwise``."""
 
-    def __init__(self, metric, stage):
+    def __init__(self, metric, stage, p=None):
         self.metric = metric
         self.stage = stage
+        self.p = p
+
+    def __call__(self, x, *args):
+        if self.stage == "expansion":
+            stats_a, stats_b, k = args
+            return _device_expand(x, stats_a, stats_b, self.metric, self.p, int(k), stages=1)
+        (k,) = args
+        return _device_expand(x, None, None, self.metric, self.p, int(k), stages=2)
 
     def __repr__(self):
-        return f"<{self.stage} of {self.metric}>"
+        return f"<device {self.stage} of {self.metric}>"
 
 
 @dataclass(frozen=True)
@@ -96,9 +105,10 @@ class SideStats:
 
 
 def _spec(name, ring, passes, norms, expansion=False, post=False, transform=None, nonneg=False, params=None):
+    p = (params or {}).get("p")
     return MetricSpec(name, ring, passes, norms,
-                      _Epilogue(name, "expansion") if expansion else None,
-                      _Epilogue(name, "post_scale") if post else None,
+                      _Epilogue(name, "expansion", p) if expansion else None,
+                      _Epilogue(name, "post_scale", p) if post else None,
                       transform, nonneg, dict(params or {}))
 
 
@@ -158,20 +168,20 @@ def _stats_layout(name):
             "jaccard": ("l0",), "euclidean": ("l2sq",)}.get(name, ())
 
 
-def expansion_apply(dots, norms_a, norms_b, spec, *, n_cols, sums_a=None, sums_b=None,
-                    dtype=np.float64, device=None):
-    """Expansion + post-scale over a dots matrix (metrics.py:287-300), on device."""
+def _device_expand(dots, stats_a, stats_b, name, p, k, stages, *, dtype=np.float64, device=None):
+    """sd_expand over a host matrix: stage 1 = expansion, 2 = post-scale, 0 = both."""
     import torch
-    name, p, strict = _metric_args(spec)
     dots = np.asarray(dots, dtype=np.float64)
-    sa = SideStats.from_norms(norms_a, signed_sum=sums_a)
-    sb = SideStats.from_norms(norms_b, signed_sum=sums_b)
+    shape = dots.shape
+    d2 = dots.reshape(1, -1) if dots.ndim == 1 else dots.reshape(-1, shape[-1]) if dots.ndim else dots.reshape(1, 1)
     tdt = _torch_dtype(dtype)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    d = torch.from_numpy(np.ascontiguousarray(dots)).to(dev).to(tdt).contiguous()
+    d = torch.from_numpy(np.ascontiguousarray(d2)).to(dev).to(tdt).contiguous()
     keep = []
 
     def arrays(st):
+        if st is None or stages == 2:
+            return None
         ptrs = []
         for attr in _stats_layout(name):
             v = st.sums(name) if attr == "signed_sum" else st.require(attr, name)
@@ -180,15 +190,26 @@ def expansion_apply(dots, norms_a, norms_b, spec, *, n_cols, sums_a=None, sums_b
             ptrs.append(t.data_ptr())
         return (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs) if ptrs else None
 
-    pa, pb = arrays(sa), arrays(sb)
+    pa, pb = arrays(stats_a), arrays(stats_b)
     flags = _lib.new_flags(dev)
-    md = _lib.metric_struct(name, p, strict)
+    md = _lib.metric_struct(name, p, True, stages=stages)
     if d.numel():
         m, n = d.shape
-        _lib.call(dev, "sd_expand", d.data_ptr(), m, n, n, _lib.dtype_code(tdt), ctypes.byref(md), int(n_cols),
+        _lib.call(dev, "sd_expand", d.data_ptr(), m, n, n, _lib.dtype_code(tdt), ctypes.byref(md), int(k),
                   pa, pb, flags.data_ptr(), _lib.stream_handle(dev))
     _lib.raise_flags(int(flags.item()), name)
-    return _lib.as_numpy_f64(d)
+    return _lib.as_numpy_f64(d).reshape(shape)
+
+
+def expansion_apply(dots, norms_a, norms_b, spec, *, n_cols, sums_a=None, sums_b=None,
+                    dtype=np.float64, device=None):
+    """Expansion + post-scale over a dots matrix (metrics.py:287-300), on device
+    in one sd_expand launch.  ``spec`` may be the reference's MetricSpec: only
+    its name and params are read (its numpy callables are never run)."""
+    name, p, strict = _metric_args(spec)
+    sa = SideStats.from_norms(norms_a, signed_sum=sums_a)
+    sb = SideStats.from_norms(norms_b, signed_sum=sums_b)
+    return _device_expand(dots, sa, sb, name, p, n_cols, stages=0, dtype=dtype, device=device)
 
 
 def _engine_report(da, db, spec_passes, name, strategy, a, b):

@@ -15,6 +15,7 @@ index) is cached on the ``DeviceCsr`` the same way the reference caches
 ``coo_row_ids`` on its matrix (sparse.py:78-81).
 """
 
+import ctypes
 from dataclasses import dataclass
 from enum import Enum
 from functools import cached_property
@@ -36,6 +37,44 @@ def _as_index(x):
 
 def _as_value(x):
     return np.ascontiguousarray(x, dtype=np.float64)
+
+
+_UFUNCS = {"add": 0, "maximum": 1, "minimum": 2, "multiply": 3}   # sd_ufunc
+
+
+def segment_reduce(values, boundaries, ufunc, identity, *, device=None):
+    """Reduce ``values`` over consecutive segments on device (sparse.py:31-53).
+
+    Segment ``t`` covers ``values[boundaries[t]:boundaries[t+1]]``; the
+    segments must tile ``values``; empty segments yield ``identity``.  The
+    device kernel associates exactly like numpy's ``ufunc.reduceat``
+    (``v[0] + pairwise_sum(v[1:])`` for add), so results are bitwise the
+    reference's.  Supported ufuncs: add, maximum, minimum, multiply.
+    """
+    import torch
+    from . import _lib
+    boundaries = np.asarray(boundaries)
+    n_segments = boundaries.size - 1
+    result = np.full(max(n_segments, 0), identity, dtype=np.float64)
+    if n_segments <= 0:
+        return result
+    values = np.asarray(values)
+    if boundaries[0] != 0 or boundaries[-1] != len(values):
+        raise ValueError("segment boundaries must tile the value array")
+    if len(values) == 0:
+        return result
+    code = _UFUNCS.get(getattr(ufunc, "__name__", ""))
+    if code is None or not isinstance(ufunc, np.ufunc):
+        raise NotImplementedError(f"segment_reduce on device supports {sorted(_UFUNCS)}, not {ufunc!r}")
+    if values.dtype != np.float32:
+        values = values.astype(np.float64)   # integer / bool sums stay exact below 2**53
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    v = torch.from_numpy(np.ascontiguousarray(values)).to(dev)
+    b = torch.from_numpy(np.ascontiguousarray(boundaries, dtype=np.int64)).to(dev)
+    out = torch.empty(n_segments, dtype=v.dtype, device=dev)
+    _lib.call(dev, "sd_segment_reduce", v.data_ptr(), int(values.size), b.data_ptr(), n_segments,
+              _lib.dtype_code(v.dtype), code, float(identity), out.data_ptr(), _lib.stream_handle(dev))
+    return out.cpu().numpy().astype(np.float64)
 
 
 @dataclass(frozen=True, eq=False)
@@ -111,10 +150,66 @@ class DegreeStats:
     histogram: np.ndarray
 
 
-def validate_and_canonicalize(indptr, indices, values, *, n_cols, n_rows=None):
+def validate_and_canonicalize(indptr, indices, values, *, n_cols, n_rows=None, device=None):
     """Check a raw CSR triple and return its canonical form (sparse.py:135-202):
     columns sorted per row, duplicates summed, zeros dropped.  Errors name the
-    offending row."""
+    offending row.  Runs on the GPU (sd_canonicalize: validation kernels, CUB
+    radix sort, duplicates summed in input order with numpy's reduceat
+    association — bitwise the reference's result); returns a host CsrMatrix."""
+    import torch
+    from . import _lib
+    indptr = _as_index(indptr)
+    indices = _as_index(indices)
+    values = _as_value(values)
+    n_rows = indptr.size - 1 if n_rows is None else int(n_rows)
+    n_cols = int(n_cols)
+    if n_rows < 0 or n_cols < 0:
+        raise ValueError("matrix dimensions must be non-negative")
+    if indptr.size != n_rows + 1:
+        raise ValueError(f"indptr length {indptr.size} does not match {n_rows} rows")
+    if indices.size != values.size:
+        raise ValueError("indices and values must have equal length")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    nnz = int(indices.size)
+    d_ptr = torch.from_numpy(indptr).to(dev)
+    d_idx = torch.from_numpy(indices).to(dev) if nnz else None
+    d_val = torch.from_numpy(values).to(dev) if nnz else None
+    o_ptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+    o_idx = torch.empty(max(1, nnz), dtype=torch.int64, device=dev)
+    o_val = torch.empty(max(1, nnz), dtype=torch.float64, device=dev)
+    out_nnz = ctypes.c_int64(0)
+    why = _lib.SdInvalid()
+    with torch.cuda.device(dev):
+        rc = _lib.load().sd_canonicalize(n_rows, n_cols, nnz, d_ptr.data_ptr(),
+                                         d_idx.data_ptr() if nnz else None, d_val.data_ptr() if nnz else None,
+                                         o_ptr.data_ptr(), o_idx.data_ptr(), o_val.data_ptr(), ctypes.byref(out_nnz),
+                                         ctypes.byref(why), _lib.stream_handle(dev))
+    if rc == _lib.SD_E_INVALID and why.kind:
+        _raise_invalid(why, nnz)
+    _lib.check(rc, "sd_canonicalize")
+    k = int(out_nnz.value)
+    return CsrMatrix(n_rows, n_cols, _ro(o_ptr.cpu().numpy()), _ro(o_idx[:k].cpu().numpy()),
+                     _ro(o_val[:k].cpu().numpy()))
+
+
+def _raise_invalid(why, nnz):
+    """sd_invalid -> the reference's exception (sparse.py:148-170)."""
+    kind = int(why.kind)
+    if kind == 1:
+        raise NegativeOffset(row=int(why.row), offset=int(why.value))
+    if kind == 2:
+        raise NonMonotonicIndptr(0, f"indptr[0] is {int(why.value)}, expected 0")
+    if kind == 3:
+        raise NonMonotonicIndptr(int(why.row), f"indptr decreases at row {int(why.row)}")
+    if kind == 4:
+        raise ValueError(f"indptr[-1] = {int(why.value)} but {nnz} entries supplied")
+    raise IndexOutOfBounds(row=int(why.row), column=int(why.column), n_cols=int(why.value))
+
+
+def canonicalize_host(indptr, indices, values, *, n_cols, n_rows=None):
+    """validate_and_canonicalize evaluated with numpy on the host: for CPU-only
+    tooling (data preparation without a GPU) and as the device version's
+    parity reference in tests/test_gpu_boundary.py."""
     indptr = _as_index(indptr)
     indices = _as_index(indices)
     values = _as_value(values)

@@ -416,3 +416,54 @@ def test_hybrid_gemm_routes(n_heavy_q):
             got = sd.pairwise_distances(a, b, sd.metric_registry(name), dtype=np.float32)
         ref = O.pairwise_distances(a, b, name)
         assert_parity(got, ref, a, b, name, np.float32, what=f"hybrid gemm {n_heavy_q}/{name}")
+
+
+# ------------------------------------------------------------ regressions
+
+def test_knn_forced_strategy_ragged_index():
+    """Forced-strategy kNN reads distance rows through their padded stride
+    (index row count not a multiple of 4)."""
+    x = _host(sd.generate(sd.GenSpec(301, 250, "zipf", zipf_s=1.3, zipf_max_degree=80, seed=71)))
+    q = sd.slice_rows(x, 0, 23)
+    spec = sd.metric_registry("manhattan")
+    ref_d, ref_i = O.kneighbors(x, q, 6, "manhattan")
+    full = O.pairwise_distances(q, x, "manhattan")
+    for strategy, rows in (("dense", 7), ("hash", 5), ("naive", 23)):
+        res = sd.kneighbors(x, q, 6, spec, strategy=strategy, batch_rows=rows)
+        assert_knn_parity(res.distances, res.indices, ref_d, ref_i, full, tol=1e-11)
+
+
+def test_hellinger_on_device_inputs():
+    """DeviceCsr inputs (sd.upload) get the sqrt value transform exactly once."""
+    rng = np.random.default_rng(72)
+    a = sd.from_dense(np.where(rng.random((12, 40)) < 0.4, rng.uniform(0.1, 2, (12, 40)), 0.0))
+    b = sd.from_dense(np.where(rng.random((30, 40)) < 0.4, rng.uniform(0.1, 2, (30, 40)), 0.0))
+    ref = O.pairwise_distances(a, b, "hellinger")
+    spec = sd.metric_registry("hellinger")
+    da = sd.upload(a.n_rows, a.n_cols, a.indptr, a.indices, a.values)
+    db = sd.upload(b.n_rows, b.n_cols, b.indptr, b.indices, b.values)
+    for x, y in ((da, db), (da, b), (a, db)):
+        for strategy in (None, "dense"):
+            got = sd.pairwise_distances(x, y, spec, strategy)
+            assert_parity(got, ref, a, b, "hellinger", np.float64, what=f"hellinger device/{strategy}")
+    ref_d, ref_i = O.kneighbors(b, a, 4, "hellinger")
+    for strategy in (None, "dense"):
+        res = sd.kneighbors(db, da, 4, spec, strategy=strategy, batch_rows=5)
+        assert_knn_parity(res.distances, res.indices, ref_d, ref_i, ref, tol=1e-11)
+    # an fp32 device matrix used at the default float64 compute dtype is converted, not misread
+    d32 = sd.upload(a.n_rows, a.n_cols, a.indptr, a.indices, np.asarray(a.values, np.float32))
+    got = sd.pairwise_distances(d32, a, sd.metric_registry("cosine"))
+    ref32 = O.pairwise_distances(a.with_values(np.asarray(a.values, np.float32).astype(np.float64)), a, "cosine")
+    np.testing.assert_allclose(got, ref32, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_forced_dense_wider_than_shared_memory(dtype):
+    """strategy='dense' with n_cols beyond one shared-memory window (column
+    windows of the staged row, engine.cu build_classes)."""
+    a = _f32(sd.generate(sd.GenSpec(20, 70000, "uniform", degree=300, seed=73)))
+    b = _f32(sd.generate(sd.GenSpec(45, 70000, "uniform", degree=300, seed=74)))
+    for name in ("manhattan", "cosine"):
+        ref = O.pairwise_distances(a, b, name)
+        got = sd.pairwise_distances(a, b, sd.metric_registry(name), "dense", dtype=dtype)
+        assert_parity(got, ref, a, b, name, dtype, what=f"wide dense {name}")
