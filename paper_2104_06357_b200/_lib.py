@@ -272,9 +272,18 @@ class DeviceIndex:
              stream_handle(dcsr.device))
         self.handle = handle
         self.n_rows = dcsr.n_rows
-        self.bytes = int(lib.sd_index_bytes(handle))
         self.tile_rows = int(lib.sd_index_tile_rows(handle))
-        self.heavy_rows = int(lib.sd_index_heavy_rows(handle))
+
+    @property
+    def bytes(self):
+        """Device memory held by the index (grows when the lazily built parts —
+        cosine postings, chebyshev masks, hybrid block — are first needed)."""
+        return int(load().sd_index_bytes(self.handle))
+
+    @property
+    def heavy_rows(self):
+        """Index rows of the hybrid heavy block (0 until the first dot-family call)."""
+        return int(load().sd_index_heavy_rows(self.handle))
 
     def __del__(self):
         try:

@@ -23,6 +23,7 @@ struct sd_index {
   int dtype = 0;
   uint32_t* colptr = nullptr;  // [n_tiles * n_cols + 1]
   void* post = nullptr;        // [nnz] Posting<T> (row id within tile, value)
+  // chebyshev (built on the first chebyshev call: ensure_cheb)
   uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
   void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
   int64_t bytes = 0;
@@ -35,6 +36,8 @@ struct sd_index {
   //
   double collide = 0.0;
   // hybrid path (hybrid.cu): rows of degree >= heavy_deg, densely as HT
+  // (built on the first dot-family call: ensure_hybrid)
+  bool hybrid_tried = false;
   int64_t heavy_deg = 0, n_heavy = 0, hpad = 0;
   int32_t* hid = nullptr;  // [n_rows]: heavy id or -1
   void* ht = nullptr;      // [n_cols][hpad] T: HT[c][h] = B[heavy row h][c]
@@ -47,5 +50,8 @@ struct sd_index {
 namespace sd {
 // hybrid.cu
 int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st);
+// isect.cu: lazily built parts of the index (thread-safe, once)
+int ensure_cheb(sd_index* ix, const sd_csr* b, cudaStream_t st);
+int ensure_hybrid(sd_index* ix, const sd_csr* b, cudaStream_t st);
 void hybrid_index_free(sd_index* ix);
 }  // namespace sd

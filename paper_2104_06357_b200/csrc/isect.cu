@@ -63,8 +63,7 @@ template <typename T>
 __global__ void index_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                      const T* __restrict__ val, int64_t n_rows, int tile, int64_t n_cols,
                                      const uint32_t* __restrict__ colptr, uint32_t* cursor,
-                                     Posting<T>* __restrict__ post, const uint8_t* __restrict__ rank,
-                                     uint8_t* __restrict__ post_rank) {
+                                     Posting<T>* __restrict__ post) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = warp; r < n_rows; r += nw) {
@@ -78,7 +77,6 @@ __global__ void index_scatter_kernel(const int64_t* __restrict__ ptr, const int3
       q.v = val[e];
       if constexpr (sizeof(T) == 8) q.pad = 0;
       post[pos] = q;
-      post_rank[pos] = rank[e];
     }
   }
 }
@@ -95,14 +93,13 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
   ix->tile = tile; ix->n_tiles = n_tiles; ix->dtype = dtype;
   auto fail = [&](int code) { sd_index_free(ix); return code; };
   const size_t ps = dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>);
+  (void)es;
   if (cudaMalloc(&ix->colptr, sizeof(uint32_t) * (n_keys + 1)) != cudaSuccess ||
-      cudaMalloc(&ix->post, ps * std::max<int64_t>(1, b->nnz)) != cudaSuccess ||
-      cudaMalloc(&ix->post_rank, std::max<int64_t>(1, b->nnz)) != cudaSuccess ||
-      cudaMalloc(&ix->topb, es * CHEB_K * std::max<int64_t>(1, b->n_rows)) != cudaSuccess) {
+      cudaMalloc(&ix->post, ps * std::max<int64_t>(1, b->nnz)) != cudaSuccess) {
     set_error("cudaMalloc failed for the inverted index");
     return fail(SD_E_CUDA);
   }
-  ix->bytes = int64_t(sizeof(uint32_t) * (n_keys + 1) + (ps + 1) * b->nnz + es * CHEB_K * b->n_rows);
+  ix->bytes = int64_t(sizeof(uint32_t) * (n_keys + 1) + ps * b->nnz);
   Scratch counts;
   if (counts.alloc(sizeof(uint32_t) * (n_keys + 1), st) != SD_OK) return fail(SD_E_CUDA);
   if (cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (n_keys + 1), st) != cudaSuccess) return fail(SD_E_CUDA);
@@ -120,15 +117,11 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
     return fail(SD_E_CUDA);
   }
   if (cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (n_keys + 1), st) != cudaSuccess) return fail(SD_E_CUDA);
-  Scratch rank;
-  if (rank.alloc(std::max<int64_t>(1, b->nnz), st) != SD_OK) return fail(SD_E_CUDA);
-  if (row_topk(b, dtype, rank.as<uint8_t>(), ix->topb, st) != SD_OK) return fail(SD_E_CUDA);
   if (b->n_rows > 0 && b->nnz > 0) {
     int rc = SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
       index_scatter_kernel<T><<<blocks, 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
                                                       b->n_rows, tile, b->n_cols, ix->colptr,
-                                                      counts.as<uint32_t>(), static_cast<Posting<T>*>(ix->post),
-                                                      rank.as<uint8_t>(), ix->post_rank);
+                                                      counts.as<uint32_t>(), static_cast<Posting<T>*>(ix->post));
       SD_LAUNCH_CHECK();
       return SD_OK;
     });
@@ -152,12 +145,76 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
     for (int64_t t = 0; t < n_tiles; ++t) { dd += h[2 * t] * h[2 * t]; sq += h[2 * t + 1]; }
     ix->collide = dd > 0.0 ? sq / dd : 0.0;
   }
-  {
-    const int rc = hybrid_index_build(b, dtype, ix, st);
-    if (rc != SD_OK) return fail(rc);
-  }
+  // the chebyshev top-K masks and the hybrid heavy-row block are built on the
+  // first call that needs them (ensure_cheb, ensure_hybrid)
   *out = ix;
   return SD_OK;
+}
+
+// rank of every posting's value in its index row (top-CHEB_K by |value|, else
+// 255), from the per-entry ranks: the posting's column follows from its
+// (tile, column) key range, its entry from a binary search in the sorted row
+template <typename T>
+__global__ void cheb_rank_kernel(const uint32_t* __restrict__ colptr, const Posting<T>* __restrict__ post,
+                                 int64_t n_keys, int64_t n_cols, int tile, const int64_t* __restrict__ bptr,
+                                 const int32_t* __restrict__ bidx, const uint8_t* __restrict__ rank,
+                                 uint8_t* __restrict__ post_rank) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n_keys; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t base = (k / n_cols) * tile;
+    const int32_t c = int32_t(k % n_cols);
+    for (uint32_t p = colptr[k]; p < colptr[k + 1]; ++p) {
+      const int64_t j = base + post[p].j;
+      int64_t lo = bptr[j], hi = bptr[j + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (bidx[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      post_rank[p] = rank[lo];
+    }
+  }
+}
+
+// Chebyshev's per-row top-CHEB_K |values| and posting ranks, once per index.
+int ensure_cheb(sd_index* ix, const sd_csr* b, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(ix->mu);
+  if (ix->topb) return SD_OK;
+  const size_t es = ix->dtype == SD_F64 ? 8 : 4;
+  void* topb = nullptr;
+  uint8_t* post_rank = nullptr;
+  if (cudaMalloc(&topb, es * CHEB_K * std::max<int64_t>(1, ix->n_rows)) != cudaSuccess ||
+      cudaMalloc(&post_rank, std::max<int64_t>(1, ix->nnz)) != cudaSuccess) {
+    if (topb) cudaFree(topb);
+    set_error("cudaMalloc failed for the chebyshev masks");
+    return SD_E_CUDA;
+  }
+  Scratch rank;
+  int rc = rank.alloc(std::max<int64_t>(1, ix->nnz), st);
+  if (rc == SD_OK) rc = row_topk(b, ix->dtype, rank.as<uint8_t>(), topb, st);
+  if (rc == SD_OK && ix->nnz > 0) {
+    const int64_t n_keys = ix->n_tiles * ix->n_cols;
+    const int blocks = int(std::min<int64_t>((n_keys + 255) / 256, int64_t(num_sms()) * 16));
+    rc = SD_DISPATCH_DTYPE(ix->dtype, T, [&]() -> int {
+      cheb_rank_kernel<T><<<std::max(1, blocks), 256, 0, st>>>(ix->colptr, static_cast<const Posting<T>*>(ix->post),
+                                                               n_keys, ix->n_cols, ix->tile, b->indptr, b->indices,
+                                                               rank.as<uint8_t>(), post_rank);
+      SD_LAUNCH_CHECK();
+      return SD_OK;
+    });
+  }
+  if (rc != SD_OK) { cudaFree(topb); cudaFree(post_rank); return rc; }
+  ix->topb = topb;
+  ix->post_rank = post_rank;
+  ix->bytes += int64_t(es * CHEB_K * ix->n_rows + ix->nnz);
+  return SD_OK;
+}
+
+// The hybrid heavy-row block, on the first dot-family call (index rows of
+// degree >= n_cols/32 held densely; hybrid.cu).
+int ensure_hybrid(sd_index* ix, const sd_csr* b, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(ix->mu);
+  if (ix->hybrid_tried) return SD_OK;
+  ix->hybrid_tried = true;
+  return hybrid_index_build(b, ix->dtype, ix, st);
 }
 
 // post_cos[p] = post[p] with the value times 1/||b_row|| (the tile of a
@@ -322,6 +379,7 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtyp
     sa->s[0] = sa_buf.ptr;
     sa->s[2] = rank;
     if (!ix_c) { set_error("chebyshev fused path needs the index"); return SD_E_INVALID; }
+    SD_TRY(ensure_cheb(const_cast<sd_index*>(ix_c), b, st));
     sb->s[0] = ix_c->topb;
     return SD_OK;
   }

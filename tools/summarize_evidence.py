@@ -1,10 +1,13 @@
-"""Copy the round's GPU evidence (gpurun_out/, scratch) into profiles/ (tracked).
+"""Copy a round's GPU evidence (gpurun_out/, scratch) into profiles/ (tracked).
 
-    python tools/summarize_evidence.py r01c
+    python tools/summarize_evidence.py r02a
+
 writes profiles/<tag>_bench_<workload>.json, <tag>_bench_ref.json,
-<tag>_launches.txt, <tag>_ncu_<kernel>.txt (key metrics + stall reasons from
-the ncu --set full text exports) and profiles/ncu_isect_traffic.json (DRAM
-bytes per launch of the fused kernel, read by bench.py for roofline.traffic).
+<tag>_launches.txt, <tag>_ncu_<workload>_<metric>_<dtype>_<kernel>.txt (key
+metrics + stall reasons of one launch, each file headed by the exact command
+that produced it) and merges the sweep kernel's DRAM bytes per launch into
+profiles/ncu_traffic.json keyed "<workload>/<metric>/<f32|f64>" — the
+`roofline.traffic` bench.py reports for the same workload, metric and dtype.
 """
 import glob
 import json
@@ -15,6 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def run(*args):
@@ -25,33 +29,42 @@ def main(tag):
     for f in glob.glob(os.path.join(OUT, "bench_*.json")):
         lines = [l for l in open(f).read().splitlines() if l.startswith("{")]
         if lines:
-            name = os.path.basename(f)
-            open(os.path.join(PROF, f"{tag}_{name}"), "w").write(lines[-1] + "\n")
+            open(os.path.join(PROF, f"{tag}_{os.path.basename(f)}"), "w").write(lines[-1] + "\n")
     if os.path.exists(os.path.join(OUT, "launches.csv")):
         txt = run("tools/summarize_launches.py", os.path.join(OUT, "launches.csv"))
         hdr = ("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)\n"
-               "# command: python bench.py --steps 3 --warmup 3 --no-cpu --no-extra  (index build included once)\n")
+               "# command: python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-check\n"
+               "# (index build and lazily built index parts included once)\n")
         open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write(hdr + txt)
+    traffic_path = os.path.join(PROF, "ncu_traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for f in sorted(glob.glob(os.path.join(OUT, "raw_*.csv"))):
-        kern = os.path.basename(f)[len("raw_"):-len(".csv")]
+        name = os.path.basename(f)[len("raw_"):-len(".csv")]      # <wl>_<metric>_<dtype>_<kernel>
+        wl, metric, dt, kernel = name.split("_", 3)
         txt = run("tools/ncu_raw.py", f)
-        hdr = (f"# ncu --set full --clock-control none --import-source on, one launch ({kern})\n"
-               "# command: python bench.py --workload c2 --metric cosine --steps 1 --warmup 1 --no-cpu --no-extra\n")
-        open(os.path.join(PROF, f"{tag}_ncu_{kern}.txt"), "w").write(hdr + txt)
-        if kern.endswith("isect_kernel"):
-            vals = {}
-            for line in txt.splitlines():
-                k, _, v = line.partition(" = ")
-                vals[k.strip()] = v.strip()
+        if not txt.strip():
+            continue
+        hdr = (f"# ncu -f --set full --clock-control none --import-source on -k regex:{kernel} -s 1 -c 1 (one launch)\n"
+               f"# command: python bench.py --workload {wl} --metric {metric} --dtype {dt} --steps 1 --warmup 1 "
+               f"--no-cpu --no-extra --no-check\n")
+        out = os.path.join(PROF, f"{tag}_ncu_{name}.txt")
+        open(out, "w").write(hdr + txt)
+        if kernel != "isect_kernel":
+            continue
+        vals = {}
+        for line in txt.splitlines():
+            k, _, v = line.partition(" = ")
+            vals[k.strip()] = v.strip()
 
-            def gb(k):
-                num, unit = vals[k].split()[:2]
-                return float(num.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-            rd, wr = gb("dram__bytes_read.sum"), gb("dram__bytes_write.sum")
-            json.dump({"kernel": "isect_kernel<float, cosine>", "workload": "c2", "dram_bytes_per_launch": rd + wr,
-                       "dram_read_bytes": rd, "dram_write_bytes": wr,
-                       "source": f"profiles/{tag}_ncu_{kern}.txt"},
-                      open(os.path.join(PROF, "ncu_isect_traffic.json"), "w"), indent=1)
+        def nbytes(k):
+            num, unit = vals[k].split()[:2]
+            return float(num.replace(",", "")) * UNITS[unit]
+        rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
+        traffic[f"{wl}/{metric}/{'f32' if dt == 'float32' else 'f64'}"] = {
+            "kernel": vals.get("Kernel Name", kernel), "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd,
+            "dram_write_bytes": wr, "duration": vals.get("gpu__time_duration.sum"),
+            "source": os.path.relpath(out, ROOT)}
+    json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
