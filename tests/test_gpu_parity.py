@@ -386,9 +386,10 @@ def test_hybrid_heavy_rows_vs_oracle(dtype):
     rows = np.sort(np.concatenate([heavy[:40], np.arange(0, idx.n_rows, 37)]))
     q = _gather_rows(idx, np.unique(rows))
     with _lib.tuned(hybrid=2):
-        ix = _lib.device_index(sd.to_device(_host(idx), dtype))
+        hidx = _host(idx)
+        ix = _lib.device_index(sd.to_device(hidx, dtype))
         assert ix.heavy_rows == 0   # the heavy block is built by the first dot-family call
-        sd.pairwise_distances(_host(q), _host(idx), sd.metric_registry("cosine"), dtype=dtype)
+        sd.pairwise_distances(_host(q), hidx, sd.metric_registry("cosine"), dtype=dtype)
         assert ix.heavy_rows == len(heavy)
         for name in DOT_FAMILY:
             a, b = (q, idx) if name not in ("dice", "jaccard", "russelrao") else (
