@@ -89,6 +89,7 @@ SIGNATURES = [
     ("sd_index_bytes", _I64, [_P]),
     ("sd_index_tile_rows", _I, [_P]),
     ("sd_index_heavy_rows", _I64, [_P]),
+    ("sd_index_hybrid_blocks", _I, [_P]),
     ("sd_pairwise", _I, [_CSR, _CSR, _P, _I, ctypes.POINTER(SdMetricDesc), ctypes.POINTER(SdStrategy),
                          _P, _I64, _P, ctypes.POINTER(SdReport), ctypes.POINTER(ctypes.c_float), _P]),
     ("sd_expand", _I, [_P, _I64, _I64, _I64, _I, ctypes.POINTER(SdMetricDesc), _I64,
@@ -284,6 +285,12 @@ class DeviceIndex:
     def heavy_rows(self):
         """Index rows of the hybrid heavy block (0 until the first dot-family call)."""
         return int(load().sd_index_heavy_rows(self.handle))
+
+    @property
+    def hybrid_blocks(self):
+        """Dense heavy-row blocks built so far: {"dot", "minsum"} subset."""
+        bits = int(load().sd_index_hybrid_blocks(self.handle))
+        return {n for b, n in ((1, "dot"), (2, "minsum")) if bits & b}
 
     def __del__(self):
         try:

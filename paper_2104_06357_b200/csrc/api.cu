@@ -174,8 +174,8 @@ static int fused_run(const sd_csr* a, const sd_csr* b, const sd_index* index, in
     SD_TRY(index_build(b, dtype, 0, &own, st));
     ix = own;
   }
-  if (topk == 0 && metric_contrib(md->metric) == C_MUL && hybrid_enabled())
-    SD_TRY(ensure_hybrid(const_cast<sd_index*>(ix), b, st));
+  if (topk == 0 && hybrid_kind(md->metric) >= 0 && hybrid_enabled())
+    SD_TRY(ensure_hybrid(const_cast<sd_index*>(ix), b, hybrid_kind(md->metric), st));
   Scratch sabuf, sbbuf;
   Stats sa, sb;
   const int ph_stats = is_namm(md->metric) ? PH_PASS2 : PH_NORMS;

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include "common.cuh"
 #include "hybrid.cuh"
+#include "tma.cuh"
 
 namespace sd {
 
@@ -43,20 +44,6 @@ __device__ __forceinline__ uint32_t kmajor_off(int r, int k, int R) {
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
   return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
          (uint64_t(1) << 46);
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(addr), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n\t.reg .pred p;\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(done) : "r"(addr), "r"(parity) : "memory");
-  }
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -94,15 +81,6 @@ __global__ void tiled_scatter_kernel(const int64_t* __restrict__ ptr, const int3
       *reinterpret_cast<uint32_t*>(blk + part + off) = lo;
     }
   }
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t addr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(addr), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
 
 // grid: (hpad / 128, 1, splits).  Warp 1 lane 0 streams stages with bulk

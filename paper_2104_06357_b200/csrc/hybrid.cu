@@ -39,18 +39,24 @@ bool hybrid_forced() { return knob(SD_TUNE_HYBRID) == 2; }
 
 // ---------------------------------------------------------------- index side
 
-// dense[idx][h] = val for the nonzeros of rows[h]: block (h, c) of a
-// (rows x chunks) grid takes every chunks-th 256-wide slice of row rows[h], so
-// a handful of long rows still spreads over the whole GPU
-template <typename T>
+// dense[(h / 128) * bstride + idx * ld + h % 128] = val for the nonzeros of
+// rows[h] (bstride = 128, ld = pad: the [n_cols][pad] image; bstride =
+// n_cols * 128, ld = 128: 128-row blocks, each [n_cols][128]); POS stores
+// max(val, 0) (the min-sum image).  Block (h, c) of a (rows x chunks) grid
+// takes every chunks-th 256-wide slice of row rows[h], so a handful of long
+// rows still spreads over the whole GPU.
+template <typename T, bool POS>
 __global__ void ht_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                   const T* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
-                                  int64_t pad, T* __restrict__ dense) {
+                                  int64_t bstride, int64_t ld, T* __restrict__ dense) {
   for (int64_t h = blockIdx.x; h < nrows; h += gridDim.x) {
     const int64_t r = rows[h];
+    T* base = dense + (h >> 7) * bstride + (h & 127);
     const int64_t step = int64_t(gridDim.y) * blockDim.x;
-    for (int64_t e = ptr[r] + int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < ptr[r + 1]; e += step)
-      dense[int64_t(idx[e]) * pad + h] = val[e];
+    for (int64_t e = ptr[r] + int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < ptr[r + 1]; e += step) {
+      const T v = val[e];
+      base[int64_t(idx[e]) * ld] = POS ? (v > T(0) ? v : T(0)) : v;
+    }
   }
 }
 
@@ -60,8 +66,8 @@ dim3 row_scatter_grid(int64_t nrows) {
   return dim3{unsigned(std::min<int64_t>(std::max<int64_t>(1, nrows), 65535)), unsigned(chunks), 1u};
 }
 
-int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st) {
-  if (!hybrid_enabled() || b->n_rows == 0 || b->nnz == 0) return SD_OK;
+// the common part: heavy ids (degree >= theta), light rows by descending degree
+static int hybrid_base_build(const sd_csr* b, sd_index* ix, cudaStream_t st) {
   const int64_t theta = hybrid_threshold(b->n_cols);
   std::vector<int64_t> ptr(b->n_rows + 1);
   SD_CUDA_TRY(cudaMemcpyAsync(ptr.data(), b->indptr, sizeof(int64_t) * (b->n_rows + 1), cudaMemcpyDeviceToHost, st));
@@ -71,33 +77,54 @@ int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st
     if (ptr[r + 1] - ptr[r] >= theta) { hid[r] = int32_t(rows.size()); rows.push_back(int32_t(r)); }
     else light.push_back(int32_t(r));
   }
+  auto deg = [&](int32_t r) { return ptr[r + 1] - ptr[r]; };
   // light rows by descending degree: the dense gather takes the long ones first
-  std::stable_sort(light.begin(), light.end(),
-                   [&](int32_t x, int32_t y) { return ptr[x + 1] - ptr[x] > ptr[y + 1] - ptr[y]; });
+  std::stable_sort(light.begin(), light.end(), [&](int32_t x, int32_t y) { return deg(x) > deg(y); });
   const int64_t nh = int64_t(rows.size());
   if (nh < 32) return SD_OK;  // nothing worth a dense block
-  const int64_t pad = (nh + 127) / 128 * 128;
-  const size_t es = dtype == SD_F64 ? 8 : 4;
-  const int64_t dense_bytes = b->n_cols * pad * int64_t(es);
-  if (dense_bytes > knob(SD_TUNE_HYBRID_MAX_MB) << 20) return SD_OK;
-  Scratch drows;
-  SD_TRY(drows.alloc(sizeof(int32_t) * nh, st));
-  if (cudaMalloc(&ix->hid, sizeof(int32_t) * b->n_rows) != cudaSuccess || cudaMalloc(&ix->ht, dense_bytes) != cudaSuccess ||
+  std::vector<int32_t> perm(nh);
+  for (int64_t h = 0; h < nh; ++h) perm[h] = int32_t(h);
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return deg(rows[x]) > deg(rows[y]); });
+  if (cudaMalloc(&ix->hid, sizeof(int32_t) * b->n_rows) != cudaSuccess ||
+      cudaMalloc(&ix->hrows, sizeof(int32_t) * nh) != cudaSuccess ||
+      cudaMalloc(&ix->hperm, sizeof(int32_t) * nh) != cudaSuccess ||
       cudaMalloc(&ix->lrows, sizeof(int32_t) * std::max<size_t>(1, light.size())) != cudaSuccess) {
     set_error("cudaMalloc failed for the hybrid index");
     return SD_E_CUDA;
   }
   SD_CUDA_TRY(cudaMemcpyAsync(ix->hid, hid.data(), sizeof(int32_t) * b->n_rows, cudaMemcpyHostToDevice, st));
-  SD_CUDA_TRY(cudaMemcpyAsync(drows.ptr, rows.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice, st));
+  SD_CUDA_TRY(cudaMemcpyAsync(ix->hrows, rows.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice, st));
+  SD_CUDA_TRY(cudaMemcpyAsync(ix->hperm, perm.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice, st));
   if (!light.empty())
     SD_CUDA_TRY(cudaMemcpyAsync(ix->lrows, light.data(), sizeof(int32_t) * light.size(), cudaMemcpyHostToDevice, st));
+  SD_CUDA_TRY(cudaStreamSynchronize(st));  // the host vectors must outlive the transfers
+  ix->heavy_deg = theta;
+  ix->n_heavy = nh;
+  ix->hpad = (nh + 127) / 128 * 128;
+  ix->n_light = int64_t(light.size());
+  ix->bytes += int64_t(sizeof(int32_t)) * (b->n_rows + 2 * nh + ix->n_light);
+  return SD_OK;
+}
+
+// dot family: HT (dense, column-major) and, for fp32, the tensor-core GEMM's
+// A-operand image
+static int hybrid_dot_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st) {
+  const int64_t nh = ix->n_heavy, pad = ix->hpad;
+  const size_t es = dtype == SD_F64 ? 8 : 4;
+  const int64_t dense_bytes = b->n_cols * pad * int64_t(es);
+  if (dense_bytes > knob(SD_TUNE_HYBRID_MAX_MB) << 20) return SD_OK;
+  if (cudaMalloc(&ix->ht, dense_bytes) != cudaSuccess) {
+    set_error("cudaMalloc failed for the hybrid index");
+    return SD_E_CUDA;
+  }
   SD_CUDA_TRY(cudaMemsetAsync(ix->ht, 0, dense_bytes, st));
   SD_TRY(SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
-    ht_scatter_kernel<T><<<row_scatter_grid(nh), 256, 0, st>>>(b->indptr, b->indices, static_cast<const T*>(b->values),
-                                                  drows.as<int32_t>(), nh, pad, static_cast<T*>(ix->ht));
+    ht_scatter_kernel<T, false><<<row_scatter_grid(nh), 256, 0, st>>>(
+        b->indptr, b->indices, static_cast<const T*>(b->values), ix->hrows, nh, 128, pad, static_cast<T*>(ix->ht));
     SD_LAUNCH_CHECK();
     return SD_OK;
   }));
+  ix->bytes += dense_bytes;
   if (dtype == SD_F32) {  // A operand image of the tensor-core GEMM
     const int64_t nks = (b->n_cols + tc_kstep() - 1) / tc_kstep();
     const int64_t tbytes = (pad / 128) * nks * 2 * 128 * tc_kstep() * 4;
@@ -105,16 +132,54 @@ int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st
       set_error("cudaMalloc failed for the hybrid index (tiled)");
       return SD_E_CUDA;
     }
-    SD_TRY(tiled_operand(b, drows.as<int32_t>(), nh, 128, nks, ix->ht_tiled, st));
+    SD_TRY(tiled_operand(b, ix->hrows, nh, 128, nks, ix->ht_tiled, st));
     ix->nks = nks;
     ix->bytes += tbytes;
   }
-  SD_CUDA_TRY(cudaStreamSynchronize(st));  // the host copies above must outlive the transfers
-  ix->heavy_deg = theta;
-  ix->n_heavy = nh;
-  ix->hpad = pad;
-  ix->n_light = int64_t(light.size());
-  ix->bytes += dense_bytes + int64_t(sizeof(int32_t)) * (b->n_rows + ix->n_light);
+  SD_CUDA_TRY(cudaStreamSynchronize(st));
+  ix->dot_ready = true;
+  return SD_OK;
+}
+
+// min-sum (manhattan): only for an index without negative (or NaN) values,
+// where |a - b| - |a| - |b| = -2 min(max(a, 0), b) for every a
+static int hybrid_minsum_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st) {
+  Scratch flag;
+  SD_TRY(flag.alloc(sizeof(unsigned int), st));
+  SD_CUDA_TRY(cudaMemsetAsync(flag.ptr, 0, sizeof(unsigned int), st));
+  SD_TRY(minsum_check_index(b, dtype, flag.as<unsigned int>(), st));
+  unsigned int bad = 0;
+  SD_CUDA_TRY(cudaMemcpyAsync(&bad, flag.ptr, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  SD_CUDA_TRY(cudaStreamSynchronize(st));
+  if (bad) return SD_OK;
+  const int64_t nch = (b->n_cols + minsum_chunk_cols(dtype) - 1) / minsum_chunk_cols(dtype);
+  const size_t bytes = sizeof(int64_t) * size_t(ix->n_heavy) * size_t(nch + 1);
+  if (cudaMalloc(&ix->hchunk, bytes) != cudaSuccess) {
+    set_error("cudaMalloc failed for the min-sum chunk pointers");
+    return SD_E_CUDA;
+  }
+  SD_TRY(minsum_chunks(b, dtype, ix->hrows, ix->n_heavy, nch, ix->hchunk, st));
+  ix->ms_nch = nch;
+  ix->bytes += int64_t(bytes);
+  ix->ms_ready = true;
+  return SD_OK;
+}
+
+int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, int kind, cudaStream_t st) {
+  if (!hybrid_enabled() || b->n_rows == 0 || b->nnz == 0) return SD_OK;
+  if (!ix->hybrid_tried) {
+    ix->hybrid_tried = true;
+    SD_TRY(hybrid_base_build(b, ix, st));
+  }
+  if (ix->n_heavy == 0) return SD_OK;
+  if (kind == HYB_DOT && !ix->dot_tried) {
+    ix->dot_tried = true;
+    return hybrid_dot_build(b, dtype, ix, st);
+  }
+  if (kind == HYB_MINSUM && !ix->ms_tried) {
+    ix->ms_tried = true;
+    return hybrid_minsum_build(b, dtype, ix, st);
+  }
   return SD_OK;
 }
 
@@ -123,7 +188,13 @@ void hybrid_index_free(sd_index* ix) {
   if (ix->ht) cudaFree(ix->ht);
   if (ix->lrows) cudaFree(ix->lrows);
   if (ix->ht_tiled) cudaFree(ix->ht_tiled);
+  if (ix->hrows) cudaFree(ix->hrows);
+  if (ix->hperm) cudaFree(ix->hperm);
+  if (ix->hchunk) cudaFree(ix->hchunk);
   ix->ht_tiled = nullptr;
+  ix->hrows = nullptr;
+  ix->hperm = nullptr;
+  ix->hchunk = nullptr;
   ix->hid = nullptr;
   ix->ht = nullptr;
   ix->lrows = nullptr;
@@ -364,17 +435,19 @@ __global__ void hreduce_kernel(const T* __restrict__ P, int splits, int64_t coun
 #endif
 constexpr int HGU = SD_HGATHER_UNROLL;
 
-// DLH[j][q] = sum_c b_jc * HQT[c][q] over light index rows j (heavy rows are
-// the GEMM's); one warp per (row, 128-wide block of heavy queries), ascending
-// column order, 8 dense rows in flight per lane.  Rows are taken from a
-// shared counter in descending-degree order (lrows, index build) so the long
-// rows start first and no warp is left with a tail of them.
-template <typename T>
+// DLH[j][q] = sum_c b_jc * HQT[c][q] (MINSUM: sum_c min(b_jc, HQT[c][q]))
+// over light index rows j (heavy rows are the dense block's); one warp per
+// (row, 128-wide block of heavy queries), ascending column order, 8 dense
+// rows in flight per lane; the block's values of column c are at
+// D + blk * bstride + c * ld.  Rows are taken from a shared counter in
+// descending-degree order (lrows, index build) so the long rows start first
+// and no warp is left with a tail of them.
+template <typename T, bool MINSUM>
 __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                       const T* __restrict__ val, const int32_t* __restrict__ lrows,
                                                       int64_t n_light, const T* __restrict__ D, int64_t ld,
-                                                      int64_t nblk, int64_t width, unsigned long long* counter,
-                                                      T* __restrict__ out) {
+                                                      int64_t bstride, int64_t nblk, int64_t ldo,
+                                                      unsigned long long* counter, T* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = (unsigned long long)(n_light * nblk);
   while (true) {
@@ -384,7 +457,7 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
     if (it >= total) break;
     const int64_t j = lrows[it / nblk], blk = int64_t(it % nblk);
     const int64_t beg = ptr[j], end = ptr[j + 1];
-    const T* dcol = D + blk * 128 + 4 * lane;
+    const T* dcol = D + blk * bstride + 4 * lane;
     T acc[4] = {T(0), T(0), T(0), T(0)};
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
       const bool ok = e0 + lane < end;
@@ -405,16 +478,17 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
         for (int u = 0; u < HGU; ++u)
           if (u0 + u < nn)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] = fma_rn(x[u], d[u][k], acc[k]);
+            for (int k = 0; k < 4; ++k)
+              acc[k] = MINSUM ? add_rn(acc[k], min_(x[u], d[u][k])) : fma_rn(x[u], d[u][k], acc[k]);
       }
     }
-    V4<T>::store_plain(out + j * ld + blk * 128 + 4 * lane, acc);
+    V4<T>::store_plain(out + j * ldo + blk * 128 + 4 * lane, acc);
   }
 }
 
 // ---------------------------------------------------------------- driver
 
-int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, HybridState& hs,
+int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, int kind, HybridState& hs,
                    cudaStream_t st) {
   hs.nhq = 0;
   const int64_t m = a->n_rows;
@@ -437,8 +511,58 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t K = a->n_cols;
   hs.qpad = (hs.nhq + 127) / 128 * 128;
+  const int64_t nblk = hs.qpad / 128;
   SD_TRY(hs.hqt.alloc(es * size_t(K) * size_t(hs.qpad), st));
   SD_CUDA_TRY(cudaMemsetAsync(hs.hqt.ptr, 0, es * size_t(K) * size_t(hs.qpad), st));
+  SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
+  SD_TRY(hs.dlh.alloc(es * size_t(std::max<int64_t>(1, b->n_rows)) * size_t(hs.qpad), st));
+  // min-sum: HQT in 128-query blocks ([blk][K][128], one contiguous stage per
+  // column chunk for the bulk copies of hminsum_kernel) holding max(a, 0)
+  const bool ms = kind == HYB_MINSUM;
+  const int64_t hq_bstride = ms ? K * 128 : 128, hq_ld = ms ? 128 : hs.qpad;
+  // the dense gather only needs HQT: it runs on a side stream, overlapping
+  // the dense block (different bottlenecks: L2 latency vs tensor pipe / TMA /
+  // shared memory) and whatever of the sweep it can share SMs with;
+  // heavy_rows joins
+  auto gather = [&](auto tag) -> int {
+    using T = decltype(tag);
+    cudaStream_t side = side_stream(0);
+    if (!side) side = st;
+    if (side != st) {
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.fork, st));
+      SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
+    }
+    int per_sm = 0;
+    if (ms) {
+      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, true>, 256, 0));
+      hgather_kernel<T, true><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
+          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
+          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+    } else {
+      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, false>, 256, 0));
+      hgather_kernel<T, false><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
+          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
+          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+    }
+    SD_LAUNCH_CHECK();
+    if (side != st) {
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.join, side));
+      hs.main = st;
+    }
+    return SD_OK;
+  };
+  if (ms) {
+    return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+      ht_scatter_kernel<T, true><<<row_scatter_grid(hs.nhq), 256, 0, st>>>(
+          a->indptr, a->indices, static_cast<const T*>(a->values), hs.hq.as<int32_t>(), hs.nhq, hq_bstride, hq_ld,
+          hs.hqt.as<T>());
+      SD_LAUNCH_CHECK();
+      SD_TRY(gather(T(0)));
+      return hminsum(ix, b, dtype, hs.hqt.ptr, K, hs.qpad, hs.part, hs.dqh.ptr, st);
+    });
+  }
   // fp32: tcgen05 3xTF32 GEMM (M = 128 heavy index rows x N = all heavy
   // queries, hgemm_tc.cu) when they fit one tile (<= 256), else mma.sync
   // 3xTF32 (tile 32 x 128 x 32); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
@@ -461,34 +585,12 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     SD_TRY(tiled_operand(a, hs.hq.as<int32_t>(), hs.nhq, int(bm), ix->nks, hs.hq_tiled.ptr, st));
   }
   SD_TRY(hs.part.alloc(es * size_t(splits) * size_t(rows) * size_t(ix->hpad), st));
-  SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
-  SD_TRY(hs.dlh.alloc(es * size_t(std::max<int64_t>(1, b->n_rows)) * size_t(hs.qpad), st));
   return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
-    ht_scatter_kernel<T><<<row_scatter_grid(hs.nhq), 256, 0, st>>>(a->indptr, a->indices, static_cast<const T*>(a->values),
-                                                  hs.hq.as<int32_t>(), hs.nhq, hs.qpad, hs.hqt.as<T>());
+    ht_scatter_kernel<T, false><<<row_scatter_grid(hs.nhq), 256, 0, st>>>(
+        a->indptr, a->indices, static_cast<const T*>(a->values), hs.hq.as<int32_t>(), hs.nhq, hq_bstride, hq_ld,
+        hs.hqt.as<T>());
     SD_LAUNCH_CHECK();
-    // the dense gather only needs HQT: it runs on a side stream, overlapping
-    // the tensor-core GEMM (different bottlenecks: L2 latency vs tensor pipe /
-    // TMA) and whatever of the sweep it can share SMs with; heavy_rows joins
-    cudaStream_t side = side_stream(0);
-    if (!side) side = st;
-    if (side != st) {
-      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));
-      SD_CUDA_TRY(cudaEventRecord(hs.fork, st));
-      SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
-    }
-    const int64_t nblk = hs.qpad / 128;
-    int per_sm = 0;
-    SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T>, 256, 0));
-    hgather_kernel<T><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
-        b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hs.qpad,
-        nblk, int64_t(hs.nhq), hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
-    SD_LAUNCH_CHECK();
-    if (side != st) {
-      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
-      SD_CUDA_TRY(cudaEventRecord(hs.join, side));
-      hs.main = st;
-    }
+    SD_TRY(gather(T(0)));
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
     if constexpr (sizeof(T) == 4) {
       if (tc5)
@@ -508,7 +610,6 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     const int64_t count = rows * ix->hpad;
     hreduce_kernel<T><<<int(std::min<int64_t>((count + 255) / 256, int64_t(num_sms()) * 16)), 256, 0, st>>>(
         hs.part.as<T>(), int(splits), count, hs.dqh.as<T>());
-    SD_LAUNCH_CHECK();
     SD_LAUNCH_CHECK();
     return SD_OK;
   });

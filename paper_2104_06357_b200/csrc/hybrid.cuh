@@ -48,8 +48,17 @@ int hgemm_tcgen05(const void* at, const void* bt, int64_t nks, int64_t hpad, int
                   float* part, cudaStream_t st);
 bool hybrid_enabled();
 bool hybrid_forced();
-// classify query rows, then GEMM + gather for the heavy ones (no-op when none)
-int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, HybridState& hs,
+// classify query rows, then the dense block (GEMM or min-sum, kind =
+// HYB_DOT / HYB_MINSUM) + gather for the heavy ones (no-op when none)
+int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, int kind, HybridState& hs,
                    cudaStream_t st);
+// hminsum.cu (manhattan): columns per chunk, index-side chunk pointers and
+// value check, and dqh[q][h] = sum_c min(HQT+[c][q], B[heavy row h][c])
+int64_t minsum_chunk_cols(int dtype);
+int minsum_check_index(const sd_csr* b, int dtype, unsigned int* flag, cudaStream_t st);
+int minsum_chunks(const sd_csr* b, int dtype, const int32_t* hrows, int64_t nh, int64_t nch, int64_t* hchunk,
+                  cudaStream_t st);
+int hminsum(const sd_index* ix, const sd_csr* b, int dtype, const void* hqt, int64_t n_cols, int64_t qpad,
+            Scratch& part, void* dqh, cudaStream_t st);
 
 }  // namespace sd

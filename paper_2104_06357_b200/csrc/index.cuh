@@ -37,21 +37,33 @@ struct sd_index {
   double collide = 0.0;
   // hybrid path (hybrid.cu): rows of degree >= heavy_deg, densely as HT
   // (built on the first dot-family call: ensure_hybrid)
+  // The common part (heavy ids, light rows) is built once; the dot-family
+  // images (HT, the GEMM operand image) and the min-sum chunk pointers on the
+  // first call of a metric that needs them.
   bool hybrid_tried = false;
   int64_t heavy_deg = 0, n_heavy = 0, hpad = 0;
   int32_t* hid = nullptr;  // [n_rows]: heavy id or -1
+  int32_t* hrows = nullptr;  // [n_heavy] index row of each heavy id
+  int32_t* hperm = nullptr;  // [n_heavy] heavy ids by descending degree (min-sum CTA balance)
+  int32_t* lrows = nullptr;  // [n_light] the other rows, by descending degree
+  int64_t n_light = 0;
+  // dot family (C_MUL)
+  bool dot_tried = false, dot_ready = false;
   void* ht = nullptr;      // [n_cols][hpad] T: HT[c][h] = B[heavy row h][c]
   void* ht_tiled = nullptr;  // fp32: HT as the tensor-core GEMM's A operand image (hgemm_tc.cu)
   int64_t nks = 0;           // its K-steps of 32 columns
-  int32_t* lrows = nullptr;  // [n_light] the other rows, by descending degree
-  int64_t n_light = 0;
+  // min-sum (C_ABS, manhattan; only when every value of B is >= 0)
+  bool ms_tried = false, ms_ready = false;
+  int64_t* hchunk = nullptr;  // [n_heavy][ms_nch + 1] first CSR entry of each column chunk (hminsum.cu)
+  int64_t ms_nch = 0;
 };
 
 namespace sd {
 // hybrid.cu
-int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st);
+enum HybridKind { HYB_DOT = 0, HYB_MINSUM = 1 };
+int hybrid_index_build(const sd_csr* b, int dtype, sd_index* ix, int kind, cudaStream_t st);
 // isect.cu: lazily built parts of the index (thread-safe, once)
 int ensure_cheb(sd_index* ix, const sd_csr* b, cudaStream_t st);
-int ensure_hybrid(sd_index* ix, const sd_csr* b, cudaStream_t st);
+int ensure_hybrid(sd_index* ix, const sd_csr* b, int kind, cudaStream_t st);
 void hybrid_index_free(sd_index* ix);
 }  // namespace sd

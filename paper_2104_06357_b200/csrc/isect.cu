@@ -208,13 +208,11 @@ int ensure_cheb(sd_index* ix, const sd_csr* b, cudaStream_t st) {
   return SD_OK;
 }
 
-// The hybrid heavy-row block, on the first dot-family call (index rows of
-// degree >= n_cols/32 held densely; hybrid.cu).
-int ensure_hybrid(sd_index* ix, const sd_csr* b, cudaStream_t st) {
+// The hybrid heavy-row block, on the first dot-family (HYB_DOT) or manhattan
+// (HYB_MINSUM) call (index rows of degree >= n_cols/32; hybrid.cu).
+int ensure_hybrid(sd_index* ix, const sd_csr* b, int kind, cudaStream_t st) {
   std::lock_guard<std::mutex> lock(ix->mu);
-  if (ix->hybrid_tried) return SD_OK;
-  ix->hybrid_tried = true;
-  return hybrid_index_build(b, ix->dtype, ix, st);
+  return hybrid_index_build(b, ix->dtype, ix, kind, st);
 }
 
 // post_cos[p] = post[p] with the value times 1/||b_row|| (the tile of a
@@ -360,9 +358,16 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int64_t* __restrict__ 
 
 // Per-row statistics of both sides for the fused epilogue (norms for the
 // dot family, one-sided sums for NAMM metrics, degrees of A for KL).
+int hybrid_kind(int metric) {
+  const int ck = metric_contrib(metric);
+  return ck == C_MUL ? HYB_DOT : ck == C_ABS ? HYB_MINSUM : -1;
+}
+
 bool isect_hybrid_eligible(const sd_index* ix, const sd_metric_desc* md, int topk) {
-  return topk == 0 && metric_contrib(md->metric) == C_MUL && ix && ix->n_heavy > 0 && hybrid_enabled() &&
-         (ix->n_tiles >= 4 || hybrid_forced());  // small indexes: the sweep is cheap, keep it exact
+  const int kind = hybrid_kind(md->metric);
+  if (topk != 0 || kind < 0 || !ix || ix->n_heavy == 0 || !hybrid_enabled()) return false;
+  if (!(kind == HYB_DOT ? ix->dot_ready : ix->ms_ready)) return false;
+  return ix->n_tiles >= 4 || hybrid_forced();  // small indexes: the sweep is cheap, keep it exact
 }
 
 int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix_c, int dtype, const sd_metric_desc* md,
@@ -440,12 +445,12 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // cosine over postings pre-divided by the index-row norms (built once per index)
   const bool cos_scaled = md->metric == SD_M_COSINE && sb.s[1] != nullptr && knob(SD_TUNE_COS_RAW) == 0;
   if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
-  // hybrid path (hybrid.cu): heavy query rows of dot-family metrics are
-  // computed densely; the sweep skips them
+  // hybrid path (hybrid.cu, hminsum.cu): heavy query rows of dot-family
+  // metrics and manhattan are computed densely; the sweep skips them
   HybridState hs;
   if (isect_hybrid_eligible(ix, md, topk)) {
     if (tm) tm->begin(PH_PASS2);
-    SD_TRY(hybrid_prepare(a, b, ix, dtype, hs, st));
+    SD_TRY(hybrid_prepare(a, b, ix, dtype, hybrid_kind(md->metric), hs, st));
     if (tm) tm->end(PH_PASS2);
   }
   if (a_stats_deferred) {
@@ -561,3 +566,4 @@ int sd_index_free(sd_index* ix) {
 int64_t sd_index_bytes(const sd_index* ix) { return ix ? ix->bytes : 0; }
 int sd_index_tile_rows(const sd_index* ix) { return ix ? ix->tile : 0; }
 int64_t sd_index_heavy_rows(const sd_index* ix) { return ix ? ix->n_heavy : 0; }
+int sd_index_hybrid_blocks(const sd_index* ix) { return ix ? (ix->dot_ready ? 1 : 0) | (ix->ms_ready ? 2 : 0) : 0; }

@@ -656,13 +656,6 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int64_t j0 = blk * JB;
     const int jn = int(tmin<int64_t>(JB, a.n - j0));
-    __syncthreads();
-    const int qp = int(qpad);
-    for (int e = threadIdx.x; e < jn * qp; e += blockDim.x) {
-      const int jj = e / qp;
-      sv[jj * qs + (e - jj * qp)] = dlh[j0 * qpad + e];
-    }
-    __syncthreads();
     // per-cell index-row data, loaded once per block row instead of once per heavy query
     constexpr int JL = 2;  // cells per lane (JB <= 64)
     int32_t hj[JL];
@@ -675,6 +668,47 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
       gb0[u] = ok && a.sb0 ? a.sb0[j0 + jj] : T(0);
       gb1[u] = ok && a.sb1 ? a.sb1[j0 + jj] : T(0);
     }
+    __syncthreads();
+    // stage the block's rows of dlh: SU vector loads in flight per thread
+    // before any shared store (a load -> store chain per element left the
+    // kernel latency-bound)
+    const int qv = int(qpad) / 4, nv = jn * qv;
+    constexpr int SU = sizeof(T) == 4 ? 8 : 4;
+    for (int v0 = threadIdx.x; v0 < nv; v0 += int(blockDim.x) * SU) {
+      T r[SU][4];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int v = v0 + u * int(blockDim.x);
+        if (v < nv) V4<T>::load(dlh + j0 * qpad + 4 * int64_t(v), r[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int v = v0 + u * int(blockDim.x);
+        if (v < nv) {
+          const int jj = v / qv, q = 4 * (v - jj * qv);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sv[jj * qs + q + t] = r[u][t];
+        }
+      }
+    }
+    __syncthreads();  // the dense-block rows below overwrite what the loop above staged for them
+    // heavy index rows of the block (no dlh row): their sums from the dense
+    // block, split over the warps by ordinal
+    {
+      int ord = 0;
+#pragma unroll
+      for (int u = 0; u < JL; ++u) {
+        unsigned mask = __ballot_sync(0xffffffffu, hj[u] >= 0);
+        while (mask) {
+          const int l = __ffs(mask) - 1;
+          mask &= mask - 1u;
+          const int32_t h = __shfl_sync(0xffffffffu, hj[u], l);
+          if (ord++ % int(blockDim.x >> 5) == warp)
+            for (int q = lane; q < nhq; q += 32) sv[(l + 32 * u) * qs + q] = dqh[int64_t(q) * hpad + h];
+        }
+      }
+    }
+    __syncthreads();
     for (int qq = warp; qq < nhq; qq += int(blockDim.x >> 5)) {
       const int64_t i = qrow[qq];
       const T ra0 = qa0[qq];
@@ -686,7 +720,9 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
       for (int u = 0; u < JL; ++u) {
         const int jj = lane + 32 * u;
         if (jj < jn) {
-          const T gv = hj[u] >= 0 ? dqh[int64_t(qq) * hpad + hj[u]] : sv[jj * qs + qq];
+          T gv = sv[jj * qs + qq];
+          // manhattan: the dense sums are sum min(a+, b); the contribution is -2x that
+          if constexpr (metric_contrib(M) == C_ABS) gv = mul_rn(T(-2), gv);
           uint32_t f = 0;
           __stcs(a.out + i * a.ldo + j0 + jj,
                  isect_cell<T, M>(a, gv, T(0), ra0, ra1, gb0[u], gb1[u], fast_zero, zero_val, f));
@@ -703,8 +739,8 @@ template <typename T, int M>
 int launch_heavy_rows(IsectArgs<T>& a, const int32_t* hq, int nhq, const int32_t* hid, const T* dqh,
                       int64_t hpad, const T* dlh, int64_t qpad, cudaStream_t st) {
   if (nhq <= 0) return SD_OK;
-  if constexpr (metric_contrib(M) != C_MUL) {
-    set_error("the hybrid path serves dot-family metrics only");
+  if constexpr (metric_contrib(M) != C_MUL && metric_contrib(M) != C_ABS) {
+    set_error("the hybrid path serves dot-family metrics and manhattan only");
     return SD_E_UNSUPPORTED;
   } else {
     const int64_t per_row = (qpad + 1) * int64_t(sizeof(T));
@@ -777,6 +813,7 @@ int launch_isect_metric(IsectArgs<T>& args, int W, cudaStream_t st) {
       case SD_M_HELLINGER: return launch_heavy_rows<T, SD_M_HELLINGER>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);      \
       case SD_M_JACCARD: return launch_heavy_rows<T, SD_M_JACCARD>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);          \
       case SD_M_RUSSELRAO: return launch_heavy_rows<T, SD_M_RUSSELRAO>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);      \
+      case SD_M_MANHATTAN: return launch_heavy_rows<T, SD_M_MANHATTAN>(a, hq, nhq, hid, dqh, hpad, dlh, qpad, st);      \
       default: set_error("metric has no hybrid path"); return SD_E_UNSUPPORTED;                                         \
     }                                                                                                                   \
   }                                                                                                                     \

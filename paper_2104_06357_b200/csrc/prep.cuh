@@ -83,6 +83,7 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype,
                 Scratch& sa_buf, Scratch& sb_buf, Stats* sa, Stats* sb, bool defer_a, cudaStream_t st);
 // could isect_run take the hybrid path (it then computes deferred query statistics)?
 bool isect_hybrid_eligible(const sd_index* ix, const sd_metric_desc* md, int topk);
+int hybrid_kind(int metric);  // HYB_DOT, HYB_MINSUM or -1 (no dense heavy-row path)
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
               void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, bool a_stats_deferred,

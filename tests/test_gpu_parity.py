@@ -405,6 +405,49 @@ def test_hybrid_heavy_rows_vs_oracle(dtype):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("n_heavy_q", [40, 300])
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_hybrid_minsum_manhattan(dtype, n_heavy_q):
+    """Manhattan's dense heavy block (hminsum.cu): with no negative index
+    value, |a-b| - |a| - |b| = -2 min(max(a,0), b), so heavy query rows are
+    summed densely (min-sum block over the index's heavy rows, min-gather over
+    its light rows).  Against the oracle and the sweep-only path; queries with
+    negative values take the max(a, 0) image; an index with a negative value
+    keeps the sweep (no min-sum block)."""
+    from paper_2104_06357_b200 import _lib
+    idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
+    deg = np.diff(np.asarray(idx.indptr))
+    heavy = np.flatnonzero(deg >= max(64, -(-idx.n_cols // 32)))
+    assert len(heavy) >= 64
+    rows = np.unique(np.concatenate([heavy[:n_heavy_q], np.arange(0, idx.n_rows, 37)]))
+    q = _gather_rows(idx, rows)
+    rng = np.random.default_rng(5)
+    signed = q.with_values(np.asarray(q.values) * np.where(rng.random(q.nnz) < 0.3, -1.0, 1.0))
+    spec = sd.metric_registry("manhattan")
+    with _lib.tuned(hybrid=2):
+        hidx = _host(idx)
+        ix = _lib.device_index(sd.to_device(hidx, dtype))
+        for a in (q, signed):
+            a = _host(a)
+            got = sd.pairwise_distances(a, hidx, spec, dtype=dtype)
+            assert "minsum" in ix.hybrid_blocks
+            ref = O.pairwise_distances(a, idx, "manhattan")
+            assert_parity(got, ref, a, idx, "manhattan", dtype, what=f"minsum {n_heavy_q}")
+            with _lib.tuned(hybrid=0):
+                sweep = sd.pairwise_distances(_host(a), _host(idx), spec, dtype=dtype)
+            assert_parity(got, sweep, a, idx, "manhattan", dtype, what="minsum vs sweep")
+        # self-distances of the sampled rows: the reference gives exactly 0
+        got = sd.pairwise_distances(_host(q), hidx, spec, dtype=dtype)
+        assert np.all(np.abs(got[np.arange(len(rows)), rows]) <= (1e-12 if dtype == np.float64 else 1e-5) *
+                      2 * np.add.reduceat(np.abs(np.asarray(q.values)), np.asarray(q.indptr)[:-1]))
+        # an index with a negative value: no min-sum block, the sweep answers
+        neg = _host(idx.with_values(np.asarray(idx.values) * np.where(np.arange(idx.nnz) == 7, -1.0, 1.0)))
+        nix = _lib.device_index(sd.to_device(neg, dtype))
+        got = sd.pairwise_distances(_host(q), neg, spec, dtype=dtype)
+        assert "minsum" not in nix.hybrid_blocks
+        assert_parity(got, O.pairwise_distances(q, neg, "manhattan"), q, neg, "manhattan", dtype, what="neg index")
+
+
 @pytest.mark.parametrize("n_heavy_q", [17, 300])
 def test_hybrid_gemm_routes(n_heavy_q):
     """The heavy block's GEMM: tcgen05 (<= 256 heavy queries, N = 32 here) and
