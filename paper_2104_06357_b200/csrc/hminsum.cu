@@ -18,11 +18,12 @@
 //     values of a chunk, HQT+[c0:c0+CW][128 queries], are one contiguous 64 KB
 //     block (HQT is stored in 128-query blocks) moved into shared memory by a
 //     single bulk copy (TMA engine) on an mbarrier, three stages in flight;
-//   * a CTA owns 64 heavy index rows (16 warps x 4, interleaved over the
-//     degree-ordered heavy ids so the warps carry similar work) and a group of
-//     consecutive chunks; for each chunk a warp walks its rows' entries of
-//     that chunk (per-(row, chunk) CSR offsets, hchunk, built once per index):
-//     32 entries per coalesced load, each broadcast by shuffle, the lane's 4
+//   * a CTA owns 64 heavy index rows (16 warps x 4, a stratified sample of
+//     the degree-ordered heavy ids so CTAs and warps carry similar work) and a
+//     group of consecutive chunks (their per-(row, chunk) CSR offsets, hchunk,
+//     built once per index, staged in shared memory); for each chunk a warp
+//     walks its rows' entries of that chunk: 32 entries per coalesced load
+//     (prefetched one chunk ahead), each broadcast by shuffle, the lane's 4
 //     query values read with one 16-byte shared load, 4 min-adds per lane
 //     into register accumulators;
 //   * partial sums per chunk group are written [group][h][q] and summed in
@@ -42,13 +43,40 @@ namespace sd {
 namespace {
 
 constexpr int MS_STAGE_BYTES = 65536;
-constexpr int MS_STAGES = 3;
+template <typename T>
+constexpr int ms_stages() { return sizeof(T) == 4 ? 3 : 2; }  // fp64: its staging area needs the room
 constexpr int MS_WARPS = 16;
 constexpr int MS_RPW = 4;                  // heavy rows per warp
 constexpr int MS_HB = MS_WARPS * MS_RPW;   // heavy rows per CTA
+constexpr int MS_MAX_G = 32;               // chunks per CTA (their pointers: 64 x 33 x 8 B of shared memory)
 
 template <typename T>
 constexpr int ms_cw() { return MS_STAGE_BYTES / (128 * int(sizeof(T))); }
+
+// acc[q] += min(x, d[q]), q < 4 — fp32 with two packed f32x2 adds (FADD2:
+// each element rounded like add.rn.f32), fp64 scalar
+__device__ __forceinline__ void minadd4(float* acc, float x, const float* d) {
+  const float m0 = fminf(x, d[0]), m1 = fminf(x, d[1]), m2 = fminf(x, d[2]), m3 = fminf(x, d[3]);
+  uint64_t a01, a23, b01, b23;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a01) : "f"(acc[0]), "f"(acc[1]));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a23) : "f"(acc[2]), "f"(acc[3]));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b01) : "f"(m0), "f"(m1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b23) : "f"(m2), "f"(m3));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a01) : "l"(b01));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a23) : "l"(b23));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[0]), "=f"(acc[1]) : "l"(a01));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[2]), "=f"(acc[3]) : "l"(a23));
+}
+__device__ __forceinline__ void minadd4(double* acc, double x, const double* d) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = __dadd_rn(acc[q], fmin(x, d[q]));
+}
+
+// one staged entry of a heavy row: byte offset of its column's query values
+// in the stage, and the index value (read back as one broadcast shared load)
+template <typename T> struct MsEntry;
+template <> struct __align__(8) MsEntry<float> { uint32_t off; float v; };
+template <> struct __align__(16) MsEntry<double> { uint32_t off, pad; double v; };
 
 // hchunk[h * (nch + 1) + k] = first entry of heavy row h with column >= k * cw
 // (k = nch: the row's end); B's rows are sorted by column (canonical CSR)
@@ -79,25 +107,39 @@ __global__ void not_nonneg_kernel(const T* __restrict__ v, int64_t n, unsigned i
 }
 
 // grid (ceil(nh / 64), groups, qpad / 128); 512 threads; dynamic shared
-// memory MS_STAGES x 64 KB.  D = HQT+ in 128-query blocks: block qb's column
-// c values at D + (qb * n_cols + c) * 128.
+// memory ms_stages x 64 KB + the CTA's chunk pointers + per-warp entry staging.  D = HQT+ in 128-query
+// blocks: block qb's column c values at D + (qb * n_cols + c) * 128.  CTA b
+// takes the degree-ordered heavy positions b, b + hblocks, b + 2 hblocks, ...
+// (a stratified sample of the degrees: every CTA carries about the same work).
 template <typename T>
 __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
     const int64_t* __restrict__ hchunk, int64_t nch, const int32_t* __restrict__ hperm, int64_t nh,
     const int32_t* __restrict__ bidx, const T* __restrict__ bval, const T* __restrict__ D, int64_t n_cols,
     int64_t G, int64_t hpad, int64_t qpad, T* __restrict__ part) {
   constexpr int CW = ms_cw<T>();
+  constexpr int MS_STAGES = ms_stages<T>();
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) unsigned long long full[MS_STAGES];
+  __shared__ __align__(8) unsigned long long full[3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t g = blockIdx.y, qb = blockIdx.z;
+  const int64_t g = blockIdx.y, qb = blockIdx.z, hb = gridDim.x;
   const int64_t k0 = g * G, k1 = tmin<int64_t>(nch, k0 + G);
+  const int gs = int(k1 - k0) + 1;  // chunk pointers per row
   const T* Dq = D + qb * n_cols * 128;
   const uint32_t sbase = uint32_t(__cvta_generic_to_shared(smem));
   const uint32_t fb = uint32_t(__cvta_generic_to_shared(&full[0]));
+  int64_t* hcs = reinterpret_cast<int64_t*>(smem + MS_STAGES * MS_STAGE_BYTES);  // [MS_HB][gs]
   if (threadIdx.x == 0) {
     for (int s = 0; s < MS_STAGES; ++s) mbar_init(fb + 8 * s, 1);
     mbar_fence_init();
+  }
+  auto heavy_of = [&](int r) -> int32_t {  // local row r = u * MS_WARPS + warp
+    const int64_t p = int64_t(r) * hb + blockIdx.x;
+    return p < nh ? hperm[p] : -1;
+  };
+  for (int e = threadIdx.x; e < MS_HB * gs; e += blockDim.x) {
+    const int r = e / gs, t = e - r * gs;
+    const int32_t h = heavy_of(r);
+    hcs[e] = h >= 0 ? hchunk[int64_t(h) * (nch + 1) + k0 + t] : 0;
   }
   __syncthreads();
   auto issue = [&](int64_t k) {
@@ -111,55 +153,84 @@ __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
     for (int64_t k = k0; k < tmin<int64_t>(k1, k0 + MS_STAGES); ++k) issue(k);
   int32_t hs[MS_RPW];
 #pragma unroll
-  for (int u = 0; u < MS_RPW; ++u) {
-    const int64_t p = int64_t(blockIdx.x) * MS_HB + u * MS_WARPS + warp;
-    hs[u] = p < nh ? hperm[p] : -1;
-  }
+  for (int u = 0; u < MS_RPW; ++u) hs[u] = heavy_of(u * MS_WARPS + warp);
+  // the first 32 entries of every row's chunk, fetched one chunk ahead so the
+  // global loads overlap the previous chunk's min-adds
+  int32_t cc[MS_RPW];
+  T cv[MS_RPW];
+  auto fetch = [&](int64_t k, int32_t* pc, T* pv) {
+#pragma unroll
+    for (int u = 0; u < MS_RPW; ++u) {
+      pc[u] = 0;
+      pv[u] = T(0);
+      if (hs[u] >= 0 && k < k1) {
+        const int64_t* hr = hcs + (u * MS_WARPS + warp) * gs + (k - k0);
+        const int64_t e = hr[0] + lane;
+        if (e < hr[1]) { pc[u] = bidx[e]; pv[u] = bval[e]; }
+      }
+    }
+  };
+  fetch(k0, cc, cv);
   T acc[MS_RPW][4];
 #pragma unroll
   for (int u = 0; u < MS_RPW; ++u)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[u][q] = T(0);
+  // per-warp staging of the prefetched entries: [MS_RPW][32]
+  MsEntry<T>* stg = reinterpret_cast<MsEntry<T>*>(hcs + MS_HB * gs) + warp * (MS_RPW * 32);
+  constexpr uint32_t ROWB = 128u * uint32_t(sizeof(T));  // bytes of one column's query values
   for (int64_t k = k0; k < k1; ++k) {
+    const int32_t c0 = int32_t(k * CW);
+    // this chunk's first 32 entries per row into the warp's staging area
+    // (padding lanes: offset 0, value 0 -> min(0, d) = 0 adds nothing)
+#pragma unroll
+    for (int u = 0; u < MS_RPW; ++u) {
+      const int64_t* hr = hcs + (u * MS_WARPS + warp) * gs + (k - k0);
+      const bool ok = hs[u] >= 0 && hr[0] + lane < hr[1];
+      MsEntry<T> en;
+      en.off = ok ? uint32_t(cc[u] - c0) * ROWB : 0u;
+      if constexpr (sizeof(T) == 8) en.pad = 0;
+      en.v = ok ? cv[u] : T(0);
+      stg[u * 32 + lane] = en;
+    }
+    __syncwarp();
+    fetch(k + 1, cc, cv);  // next chunk's entries: in flight during this chunk
     const int s = int((k - k0) % MS_STAGES);
     mbar_wait(fb + 8 * s, uint32_t(((k - k0) / MS_STAGES) & 1));
     const uint32_t sq = sbase + uint32_t(s) * MS_STAGE_BYTES + uint32_t(lane) * 4u * uint32_t(sizeof(T));
-    const int32_t c0 = int32_t(k * CW);
 #pragma unroll
     for (int u = 0; u < MS_RPW; ++u) {
       if (hs[u] < 0) continue;  // warp-uniform
-      const int64_t* hc = hchunk + int64_t(hs[u]) * (nch + 1) + k;
-      const int64_t beg = hc[0], end = hc[1];
-      for (int64_t e0 = beg; e0 < end; e0 += 32) {
-        const bool ok = e0 + lane < end;
-        const int32_t cl = ok ? bidx[e0 + lane] - c0 : 0;
-        const T vl = ok ? bval[e0 + lane] : T(0);
-        const int nn = int(tmin<int64_t>(32, end - e0));
-        int t = 0;
-        for (; t + 4 <= nn; t += 4) {
-          T d[4][4], x[4];
+      const int64_t* hr = hcs + (u * MS_WARPS + warp) * gs + (k - k0);
+      const int64_t beg = hr[0], end = hr[1];
+      const int nn = int(tmin<int64_t>(32, end - beg));
+      const MsEntry<T>* row = stg + u * 32;
+      for (int t = 0; t < nn; t += 4) {  // padded to a multiple of 4
+        T d[4][4];
+        MsEntry<T> en[4];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int32_t c = __shfl_sync(0xffffffffu, cl, t + v);
-            x[v] = __shfl_sync(0xffffffffu, vl, t + v);
-            lds4(sq + uint32_t(c) * 128u * uint32_t(sizeof(T)), d[v]);
-          }
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[u][q] = add_rn(acc[u][q], min_(x[v], d[v][q]));
+        for (int v = 0; v < 4; ++v) {
+          en[v] = row[t + v];
+          lds4(sq + en[v].off, d[v]);
         }
-        for (; t < nn; ++t) {
-          T d[4];
-          const int32_t c = __shfl_sync(0xffffffffu, cl, t);
-          const T x = __shfl_sync(0xffffffffu, vl, t);
-          lds4(sq + uint32_t(c) * 128u * uint32_t(sizeof(T)), d);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[u][q] = add_rn(acc[u][q], min_(x, d[q]));
+        for (int v = 0; v < 4; ++v) minadd4(acc[u], en[v].v, d[v]);
+      }
+      for (int64_t e0 = beg + 32; e0 < end; e0 += 32) {  // long rows: entries beyond the staged 32
+        const bool ok = e0 + lane < end;
+        const uint32_t ol = ok ? uint32_t(bidx[e0 + lane] - c0) * ROWB : 0u;
+        const T vl = ok ? bval[e0 + lane] : T(0);
+        const int n2 = int(tmin<int64_t>(32, end - e0));
+        for (int t = 0; t < n2; ++t) {
+          T d[4];
+          const uint32_t o = __shfl_sync(0xffffffffu, ol, t);
+          const T x = __shfl_sync(0xffffffffu, vl, t);
+          lds4(sq + o, d);
+          minadd4(acc[u], x, d);
         }
       }
     }
-    __syncthreads();  // every warp is done with stage s
+    __syncthreads();  // every warp is done with stage s (and its staging area)
     if (threadIdx.x == 0 && k + MS_STAGES < k1) issue(k + MS_STAGES);
   }
   T* out = part + g * hpad * qpad + qb * 128 + 4 * lane;
@@ -209,15 +280,28 @@ int hminsum(const sd_index* ix, const sd_csr* b, int dtype, const void* hqt, int
             Scratch& part, void* dqh, cudaStream_t st) {
   const int64_t nh = ix->n_heavy, nch = ix->ms_nch;
   const int64_t hblocks = (nh + MS_HB - 1) / MS_HB, qblocks = qpad / 128;
-  // chunk groups: about 4 waves of one-CTA-per-SM blocks (fewer partials than
-  // one group per chunk, enough CTAs to balance)
-  const int64_t want = std::max<int64_t>(1, (4 * int64_t(num_sms()) + hblocks * qblocks - 1) / (hblocks * qblocks));
-  const int64_t G = std::max<int64_t>(MS_STAGES, (nch + want - 1) / want);
-  const int64_t groups = (nch + G - 1) / G;
+  // chunk groups: 3-6 waves of one-CTA-per-SM blocks (fewer partials than
+  // one group per chunk, enough CTAs to balance), the count whose last wave
+  // is fullest; at most MS_MAX_G chunks per group (their pointers sit in
+  // shared memory)
+  const int64_t sms = num_sms(), per = hblocks * qblocks;
+  int64_t groups = 0;
+  double best = 1e30;
+  for (int64_t gg = std::max<int64_t>(1, (3 * sms) / per); gg <= std::max<int64_t>(1, (6 * sms + per - 1) / per); ++gg) {
+    const int64_t G0 = (nch + gg - 1) / gg;
+    if (G0 > MS_MAX_G) continue;
+    const int64_t ctas = per * ((nch + G0 - 1) / G0);
+    const double waste = double((ctas + sms - 1) / sms * sms) / double(ctas);
+    if (waste < best - 1e-9) { best = waste; groups = gg; }
+  }
+  if (groups == 0) groups = (nch + MS_MAX_G - 1) / MS_MAX_G;
+  const int64_t G = (nch + groups - 1) / groups;
+  groups = (nch + G - 1) / G;
   const size_t es = dtype == SD_F64 ? 8 : 4;
   SD_TRY(part.alloc(es * size_t(groups) * size_t(ix->hpad) * size_t(qpad), st));
-  const size_t smem = size_t(MS_STAGES) * MS_STAGE_BYTES;
   return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    const size_t smem = size_t(ms_stages<T>()) * MS_STAGE_BYTES + size_t(MS_HB) * size_t(G + 1) * sizeof(int64_t) +
+                        size_t(MS_WARPS) * MS_RPW * 32 * sizeof(MsEntry<T>);
     SD_TRY(prepare_smem(hminsum_kernel<T>, smem, "hminsum_kernel"));
     const dim3 grid{unsigned(hblocks), unsigned(groups), unsigned(qblocks)};
     hminsum_kernel<T><<<grid, MS_WARPS * 32, smem, st>>>(ix->hchunk, nch, ix->hperm, nh, b->indices,

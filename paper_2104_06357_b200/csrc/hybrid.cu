@@ -203,7 +203,7 @@ void hybrid_index_free(sd_index* ix) {
 // ---------------------------------------------------------------- query side
 
 // non-blocking side streams per device (created once, never destroyed):
-// 0 carries the dense gather, 1 the deferred query statistics
+// 0 carries the dense gather, 1 the deferred query statistics and work plan
 cudaStream_t side_stream(int which) {
   static std::mutex mu;
   static cudaStream_t streams[2][64] = {};
@@ -211,7 +211,12 @@ cudaStream_t side_stream(int which) {
   if (which < 0 || which > 1 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
   cudaStream_t& s = streams[which][dev];
-  if (!s && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
+  // highest priority: the side streams carry latency-bound work (gather,
+  // statistics, work plan) that should be dispatched onto free SM resources
+  // ahead of the pending CTAs of the dense block on the caller's stream
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) hi = 0;
+  if (!s && cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess) s = nullptr;
   return s;
 }
 
@@ -488,8 +493,7 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
 
 // ---------------------------------------------------------------- driver
 
-int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, int kind, HybridState& hs,
-                   cudaStream_t st) {
+int hybrid_classify(const sd_csr* a, const sd_index* ix, HybridState& hs, cudaStream_t st) {
   hs.nhq = 0;
   const int64_t m = a->n_rows;
   const int cap = int(std::max<int64_t>(1, knob(SD_TUNE_HYBRID_MAX_QUERIES)));
@@ -503,10 +507,18 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   classify_kernel<<<std::max(1, blocks), 256, 0, st>>>(a->indptr, m, ix->heavy_deg, cap, hs.qid.as<int32_t>(),
                                                        hs.hq.as<int32_t>(), hs.count.as<unsigned int>());
   SD_LAUNCH_CHECK();
+  hs.cap = cap;
+  return SD_OK;
+}
+
+int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, int kind, HybridState& hs,
+                   cudaStream_t st) {
+  // the host needs the heavy count to size the dense block: one small read
+  // (work queued on the side streams before it keeps the GPU busy meanwhile)
   unsigned int cnt = 0;
   SD_CUDA_TRY(cudaMemcpyAsync(&cnt, hs.count.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, st));
   SD_CUDA_TRY(cudaStreamSynchronize(st));
-  hs.nhq = int(std::min<unsigned int>(cnt, unsigned(cap)));
+  hs.nhq = int(std::min<unsigned int>(cnt, unsigned(hs.cap)));
   if (hs.nhq == 0) return SD_OK;
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t K = a->n_cols;
@@ -520,10 +532,8 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   // column chunk for the bulk copies of hminsum_kernel) holding max(a, 0)
   const bool ms = kind == HYB_MINSUM;
   const int64_t hq_bstride = ms ? K * 128 : 128, hq_ld = ms ? 128 : hs.qpad;
-  // the dense gather only needs HQT: it runs on a side stream, overlapping
-  // the dense block (different bottlenecks: L2 latency vs tensor pipe / TMA /
-  // shared memory) and whatever of the sweep it can share SMs with;
-  // heavy_rows joins
+  // the dense gather runs on a side stream (heavy_rows joins it), after the
+  // dense block
   auto gather = [&](auto tag) -> int {
     using T = decltype(tag);
     cudaStream_t side = side_stream(0);
@@ -534,6 +544,17 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
       SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
     }
     int per_sm = 0;
+    // keep the SMs' shared-memory carveout at its maximum while the gather
+    // runs, so the dense block's CTAs (~200 KB of stages) co-reside with it
+    // instead of waiting for SMs to drain
+    static const bool carve = [] {
+      cudaFuncSetAttribute(hgather_kernel<float, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(hgather_kernel<float, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(hgather_kernel<double, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(hgather_kernel<double, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      return true;
+    }();
+    (void)carve;
     if (ms) {
       SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, true>, 256, 0));
       hgather_kernel<T, true><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
@@ -590,7 +611,6 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
         a->indptr, a->indices, static_cast<const T*>(a->values), hs.hq.as<int32_t>(), hs.nhq, hq_bstride, hq_ld,
         hs.hqt.as<T>());
     SD_LAUNCH_CHECK();
-    SD_TRY(gather(T(0)));
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
     if constexpr (sizeof(T) == 4) {
       if (tc5)
@@ -607,6 +627,11 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
                                                    ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());
     }
     SD_LAUNCH_CHECK();
+    // the gather forks after the GEMM: run side by side they slow each other
+    // down (C2: 550 us together vs 202 + 244 us in sequence; the GEMM streams
+    // its operand image from HBM, the gather is L2-latency bound), and the
+    // side stream's priority would otherwise put the gather first
+    SD_TRY(gather(T(0)));
     const int64_t count = rows * ix->hpad;
     hreduce_kernel<T><<<int(std::min<int64_t>((count + 255) / 256, int64_t(num_sms()) * 16)), 256, 0, st>>>(
         hs.part.as<T>(), int(splits), count, hs.dqh.as<T>());

@@ -10,7 +10,8 @@ struct HybridState {
   cudaEvent_t fork = nullptr;  // the gather's side-stream fork / join (hybrid_prepare)
   cudaEvent_t join = nullptr;
   cudaStream_t main = nullptr;  // the caller's stream (scratch below is freed on it)
-  cudaEvent_t stats_done = nullptr;  // deferred query statistics (isect_run) finished
+  cudaEvent_t cls = nullptr;         // classification done (side-stream plan / statistics start)
+  cudaEvent_t stats_done = nullptr;  // deferred query statistics + work plan (isect_run) finished
   // the caller's stream waits for the side stream (before heavy_rows and
   // before any of this state's scratch is released on it)
   int wait(cudaStream_t st) {
@@ -19,11 +20,14 @@ struct HybridState {
   }
   ~HybridState() {  // runs before the Scratch members free their buffers on `main`
     if (join && main) cudaStreamWaitEvent(main, join, 0);
+    if (stats_done && main) cudaStreamWaitEvent(main, stats_done, 0);
     if (fork) cudaEventDestroy(fork);
+    if (cls) cudaEventDestroy(cls);
     if (stats_done) cudaEventDestroy(stats_done);
     if (join) cudaEventDestroy(join);
   }
   int nhq = 0;          // heavy query rows of this call (ids 0..nhq-1)
+  int cap = 0;          // most heavy query rows one call takes
   int64_t qpad = 0;     // nhq rounded up to 128
   Scratch qid;          // [m] heavy id of each query row or -1
   Scratch hq;           // [cap] query row of each heavy id
@@ -48,7 +52,9 @@ int hgemm_tcgen05(const void* at, const void* bt, int64_t nks, int64_t hpad, int
                   float* part, cudaStream_t st);
 bool hybrid_enabled();
 bool hybrid_forced();
-// classify query rows, then the dense block (GEMM or min-sum, kind =
+// classify query rows (heavy ids in hs.qid / hs.hq, count on the device) ...
+int hybrid_classify(const sd_csr* a, const sd_index* ix, HybridState& hs, cudaStream_t st);
+// ... then read the count and run the dense block (GEMM or min-sum, kind =
 // HYB_DOT / HYB_MINSUM) + gather for the heavy ones (no-op when none)
 int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, int kind, HybridState& hs,
                    cudaStream_t st);

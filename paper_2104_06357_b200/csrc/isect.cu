@@ -447,35 +447,21 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   if (cos_scaled) SD_TRY(ensure_post_cos(const_cast<sd_index*>(ix), sb.s[1], st));
   // hybrid path (hybrid.cu, hminsum.cu): heavy query rows of dot-family
   // metrics and manhattan are computed densely; the sweep skips them
+  // (declared before the hybrid state: its destructor makes the caller's
+  // stream wait for the side streams before these buffers are released)
+  Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
   HybridState hs;
-  if (isect_hybrid_eligible(ix, md, topk)) {
-    if (tm) tm->begin(PH_PASS2);
-    SD_TRY(hybrid_prepare(a, b, ix, dtype, hybrid_kind(md->metric), hs, st));
-    if (tm) tm->end(PH_PASS2);
-  }
-  if (a_stats_deferred) {
-    // the query statistics are only needed by the sweep and the heavy-row
-    // epilogue: on the hybrid path they run on a second side stream,
-    // overlapping the GEMM and the gather
-    cudaStream_t ss = hs.fork ? side_stream(1) : nullptr;
-    if (ss) SD_CUDA_TRY(cudaStreamWaitEvent(ss, hs.fork, 0));
-    Stats tmp;
-    SD_TRY(metric_stats(a, dtype, md, true, const_cast<void*>(sa.s[0]), &tmp, ss ? ss : st));
-    if (ss) {
-      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.stats_done, cudaEventDisableTiming));
-      SD_CUDA_TRY(cudaEventRecord(hs.stats_done, ss));
-      SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.stats_done, 0));
-    }
-  }
+  const bool hyb = isect_hybrid_eligible(ix, md, topk);
+  if (hyb) SD_TRY(hybrid_classify(a, ix, hs, st));
   const int64_t be0 = knob(SD_TUNE_ISECT_BAND);
   // bytes the sweep streams: postings + their (tile, column) ranges (not the
   // hybrid block or the other metric's posting copy, which it never touches)
   const int64_t post_bytes = std::max<int64_t>(
       1, ix->nnz * int64_t(dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>)) +
              int64_t(sizeof(uint32_t)) * (ix->n_tiles * ix->n_cols + 1));
-  // once the hybrid path has taken the heavy query rows, a band's postings
-  // take about a fifth of the L2 (C2 cosine: bands of 100 MB 2.37 ms, 50 MB
-  // 2.28, 25 MB 2.21, 12 MB 2.43) — the rest holds the streaming output.
+  // once the hybrid path takes the heavy query rows, a band's postings take
+  // about a fifth of the L2 (C2 cosine: bands of 100 MB 2.37 ms, 50 MB 2.28,
+  // 25 MB 2.21, 12 MB 2.43) — the rest holds the streaming output.
   // Otherwise whole-L2 bands: with heavy rows in the sweep (C2 manhattan 4.9
   // vs 5.9 ms) and for kNN, where every band adds a top-k list per query to
   // merge (C5: 49 vs 56 ms), smaller bands cost more than they save.
@@ -483,13 +469,12 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // Dense-ish indexes (long posting lists per (tile, column), C4: ~280) also
   // prefer the small bands (C4 46.4 -> 39.6 ms).
   const bool long_lists = ix->nnz > 64 * ix->n_tiles * ix->n_cols;
-  const int64_t div = ld > 0 ? ld : (topk == 0 && (hs.nhq > 0 || long_lists) ? 5 : 1);
+  const int64_t div = ld > 0 ? ld : (topk == 0 && (hyb || long_lists) ? 5 : 1);
   const int64_t band_bytes = std::max<int64_t>(1, l2_bytes() / std::max<int64_t>(1, div));
   const int64_t n_bands0 = (post_bytes + band_bytes - 1) / band_bytes;
   const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
   const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 > 0 ? be0 : auto_band));
   const int64_t max_items = m * band0 * ((ix->n_tiles + band0 - 1) / band0);
-  Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
   SD_TRY(order.alloc(sizeof(int32_t) * m, st));
   SD_TRY(tpi.alloc(sizeof(int32_t) * m, st));
   SD_TRY(item_off.alloc(sizeof(int64_t) * (m + 1), st));
@@ -497,11 +482,40 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   SD_TRY(counter.alloc(sizeof(unsigned int), st));
   SD_CUDA_TRY(cudaMemsetAsync(counter.ptr, 0, sizeof(unsigned int), st));
   const int64_t band = band0;
-  plan_kernel<<<1, 1024, 0, st>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
-                                  hs.nhq > 0 ? hs.qid.as<int32_t>() : nullptr,
+  // On the hybrid path the work plan and the deferred query statistics only
+  // need the classification: they run on a side stream, off the critical
+  // path (the host's read of the heavy count, the dense block and the gather
+  // proceed meanwhile); the sweep waits for them.
+  cudaStream_t ps = st;
+  if (hyb) {
+    cudaStream_t s1 = side_stream(1);
+    if (s1) {
+      ps = s1;
+      hs.main = st;
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.cls, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.cls, st));
+      SD_CUDA_TRY(cudaStreamWaitEvent(ps, hs.cls, 0));
+    }
+  }
+  if (a_stats_deferred) {
+    Stats tmp;
+    SD_TRY(metric_stats(a, dtype, md, true, const_cast<void*>(sa.s[0]), &tmp, ps));
+  }
+  plan_kernel<<<1, 1024, 0, ps>>>(a->indptr, m, ix->n_tiles, band, warps, ix->tile / 16, tile_major,
+                                  hyb ? hs.qid.as<int32_t>() : nullptr,
                                   order.as<int32_t>(), tpi.as<int32_t>(), item_off.as<int64_t>(),
                                   item_pos.as<int32_t>());
   SD_LAUNCH_CHECK();
+  if (ps != st) {
+    SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.stats_done, cudaEventDisableTiming));
+    SD_CUDA_TRY(cudaEventRecord(hs.stats_done, ps));
+  }
+  if (hyb) {
+    if (tm) tm->begin(PH_PASS2);
+    SD_TRY(hybrid_prepare(a, b, ix, dtype, hybrid_kind(md->metric), hs, st));
+    if (tm) tm->end(PH_PASS2);
+  }
+  if (ps != st) SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.stats_done, 0));
   if (topk > 0) {
     SD_TRY(cand_d.alloc(es * size_t(max_items) * topk, st));
     SD_TRY(cand_i.alloc(sizeof(int64_t) * size_t(max_items) * topk, st));
