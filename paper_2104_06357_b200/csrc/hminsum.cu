@@ -48,6 +48,7 @@ constexpr int ms_stages() { return sizeof(T) == 4 ? 3 : 2; }  // fp64: its stagi
 constexpr int MS_WARPS = 16;
 constexpr int MS_RPW = 4;                  // heavy rows per warp
 constexpr int MS_HB = MS_WARPS * MS_RPW;   // heavy rows per CTA
+constexpr int MS_UNROLL = 8;               // staged entries per step (rows padded to a multiple)
 constexpr int MS_MAX_G = 32;               // chunks per CTA (their pointers: 64 x 33 x 8 B of shared memory)
 
 template <typename T>
@@ -112,24 +113,27 @@ __global__ void not_nonneg_kernel(const T* __restrict__ v, int64_t n, unsigned i
 // takes the degree-ordered heavy positions b, b + hblocks, b + 2 hblocks, ...
 // (a stratified sample of the degrees: every CTA carries about the same work).
 template <typename T>
-__global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
+__global__ void __launch_bounds__((MS_WARPS + 1) * 32, 1) hminsum_kernel(
     const int64_t* __restrict__ hchunk, int64_t nch, const int32_t* __restrict__ hperm, int64_t nh,
     const int32_t* __restrict__ bidx, const T* __restrict__ bval, const T* __restrict__ D, int64_t n_cols,
     int64_t G, int64_t hpad, int64_t qpad, T* __restrict__ part) {
   constexpr int CW = ms_cw<T>();
   constexpr int MS_STAGES = ms_stages<T>();
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) unsigned long long full[3];
+  __shared__ __align__(8) unsigned long long bars[6];  // full[3], empty[3]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = blockIdx.y, qb = blockIdx.z, hb = gridDim.x;
   const int64_t k0 = g * G, k1 = tmin<int64_t>(nch, k0 + G);
   const int gs = int(k1 - k0) + 1;  // chunk pointers per row
   const T* Dq = D + qb * n_cols * 128;
   const uint32_t sbase = uint32_t(__cvta_generic_to_shared(smem));
-  const uint32_t fb = uint32_t(__cvta_generic_to_shared(&full[0]));
+  const uint32_t fb = uint32_t(__cvta_generic_to_shared(&bars[0])), eb = fb + 24;
   int64_t* hcs = reinterpret_cast<int64_t*>(smem + MS_STAGES * MS_STAGE_BYTES);  // [MS_HB][gs]
   if (threadIdx.x == 0) {
-    for (int s = 0; s < MS_STAGES; ++s) mbar_init(fb + 8 * s, 1);
+    for (int s = 0; s < MS_STAGES; ++s) {
+      mbar_init(fb + 8 * s, 1);
+      mbar_init(eb + 8 * s, MS_WARPS);
+    }
     mbar_fence_init();
   }
   auto heavy_of = [&](int r) -> int32_t {  // local row r = u * MS_WARPS + warp
@@ -142,15 +146,23 @@ __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
     hcs[e] = h >= 0 ? hchunk[int64_t(h) * (nch + 1) + k0 + t] : 0;
   }
   __syncthreads();
-  auto issue = [&](int64_t k) {
-    const int s = int((k - k0) % MS_STAGES);
-    const int64_t c0 = k * CW;
-    const uint32_t bytes = uint32_t(tmin<int64_t>(CW, n_cols - c0)) * 128u * uint32_t(sizeof(T));
-    mbar_expect_tx(fb + 8 * s, bytes);
-    bulk_g2s(sbase + uint32_t(s) * MS_STAGE_BYTES, Dq + c0 * 128, bytes, fb + 8 * s);
-  };
-  if (threadIdx.x == 0)
-    for (int64_t k = k0; k < tmin<int64_t>(k1, k0 + MS_STAGES); ++k) issue(k);
+  if (warp == MS_WARPS) {
+    // producer warp: refills a stage once all consumer warps released it, so
+    // the consumers drift apart by up to MS_STAGES - 1 chunks instead of
+    // meeting at a block-wide barrier every chunk
+    if (lane == 0) {
+      for (int64_t k = k0; k < k1; ++k) {
+        const int64_t i = k - k0;
+        const int s = int(i % MS_STAGES);
+        if (i >= MS_STAGES) mbar_wait(eb + 8 * s, uint32_t(((i / MS_STAGES) - 1) & 1));
+        const int64_t c0 = k * CW;
+        const uint32_t bytes = uint32_t(tmin<int64_t>(CW, n_cols - c0)) * 128u * uint32_t(sizeof(T));
+        mbar_expect_tx(fb + 8 * s, bytes);
+        bulk_g2s(sbase + uint32_t(s) * MS_STAGE_BYTES, Dq + c0 * 128, bytes, fb + 8 * s);
+      }
+    }
+    return;
+  }
   int32_t hs[MS_RPW];
 #pragma unroll
   for (int u = 0; u < MS_RPW; ++u) hs[u] = heavy_of(u * MS_WARPS + warp);
@@ -183,6 +195,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
     const int32_t c0 = int32_t(k * CW);
     // this chunk's first 32 entries per row into the warp's staging area
     // (padding lanes: offset 0, value 0 -> min(0, d) = 0 adds nothing)
+    __syncwarp();  // the previous chunk's reads of the staging area are done
 #pragma unroll
     for (int u = 0; u < MS_RPW; ++u) {
       const int64_t* hr = hcs + (u * MS_WARPS + warp) * gs + (k - k0);
@@ -195,8 +208,9 @@ __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
     }
     __syncwarp();
     fetch(k + 1, cc, cv);  // next chunk's entries: in flight during this chunk
-    const int s = int((k - k0) % MS_STAGES);
-    mbar_wait(fb + 8 * s, uint32_t(((k - k0) / MS_STAGES) & 1));
+    const int64_t i = k - k0;
+    const int s = int(i % MS_STAGES);
+    mbar_wait(fb + 8 * s, uint32_t((i / MS_STAGES) & 1));
     const uint32_t sq = sbase + uint32_t(s) * MS_STAGE_BYTES + uint32_t(lane) * 4u * uint32_t(sizeof(T));
 #pragma unroll
     for (int u = 0; u < MS_RPW; ++u) {
@@ -205,16 +219,16 @@ __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
       const int64_t beg = hr[0], end = hr[1];
       const int nn = int(tmin<int64_t>(32, end - beg));
       const MsEntry<T>* row = stg + u * 32;
-      for (int t = 0; t < nn; t += 4) {  // padded to a multiple of 4
-        T d[4][4];
-        MsEntry<T> en[4];
+      for (int t = 0; t < nn; t += MS_UNROLL) {  // padded to a multiple of MS_UNROLL
+        T d[MS_UNROLL][4];
+        MsEntry<T> en[MS_UNROLL];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
+        for (int v = 0; v < MS_UNROLL; ++v) {
           en[v] = row[t + v];
           lds4(sq + en[v].off, d[v]);
         }
 #pragma unroll
-        for (int v = 0; v < 4; ++v) minadd4(acc[u], en[v].v, d[v]);
+        for (int v = 0; v < MS_UNROLL; ++v) minadd4(acc[u], en[v].v, d[v]);
       }
       for (int64_t e0 = beg + 32; e0 < end; e0 += 32) {  // long rows: entries beyond the staged 32
         const bool ok = e0 + lane < end;
@@ -230,8 +244,8 @@ __global__ void __launch_bounds__(MS_WARPS * 32, 1) hminsum_kernel(
         }
       }
     }
-    __syncthreads();  // every warp is done with stage s (and its staging area)
-    if (threadIdx.x == 0 && k + MS_STAGES < k1) issue(k + MS_STAGES);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(eb + 8 * s);  // this warp is done with stage s
   }
   T* out = part + g * hpad * qpad + qb * 128 + 4 * lane;
 #pragma unroll
@@ -304,7 +318,7 @@ int hminsum(const sd_index* ix, const sd_csr* b, int dtype, const void* hqt, int
                         size_t(MS_WARPS) * MS_RPW * 32 * sizeof(MsEntry<T>);
     SD_TRY(prepare_smem(hminsum_kernel<T>, smem, "hminsum_kernel"));
     const dim3 grid{unsigned(hblocks), unsigned(groups), unsigned(qblocks)};
-    hminsum_kernel<T><<<grid, MS_WARPS * 32, smem, st>>>(ix->hchunk, nch, ix->hperm, nh, b->indices,
+    hminsum_kernel<T><<<grid, (MS_WARPS + 1) * 32, smem, st>>>(ix->hchunk, nch, ix->hperm, nh, b->indices,
                                                          static_cast<const T*>(b->values), static_cast<const T*>(hqt),
                                                          n_cols, G, ix->hpad, qpad, part.as<T>());
     SD_LAUNCH_CHECK();
