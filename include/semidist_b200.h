@@ -151,7 +151,9 @@ typedef enum {
   SD_TUNE_HYBRID_MAX_MB = 8,   /* SD_HYBRID_MAX_MB: largest dense heavy block (MiB) */
   SD_TUNE_HYBRID_MAX_QUERIES = 9, /* SD_HYBRID_MAX_QUERIES: heavy query rows per call */
   SD_TUNE_HGEMM = 10,          /* SD_HGEMM: 0 automatic, 1 CUDA-core, 2 mma.sync */
-  SD_TUNE_COUNT = 11
+  SD_TUNE_DENSE = 11,          /* SD_DENSE: dense-index tensor-core mode, 0 off, 1 automatic, 2 forced */
+  SD_TUNE_DENSE_MAX_MB = 12,   /* SD_DENSE_MAX_MB: largest dense index image (MiB) */
+  SD_TUNE_COUNT = 13
 } sd_tune_knob;
 
 /* ---------------------------------------------------------------- misc */

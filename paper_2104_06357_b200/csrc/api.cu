@@ -43,6 +43,8 @@ static void init_knobs() {
   g_knobs[SD_TUNE_HYBRID] = env("SD_HYBRID", 1);
   g_knobs[SD_TUNE_HYBRID_MAX_MB] = env("SD_HYBRID_MAX_MB", 1024);
   g_knobs[SD_TUNE_HYBRID_MAX_QUERIES] = env("SD_HYBRID_MAX_QUERIES", 1024);
+  g_knobs[SD_TUNE_DENSE] = env("SD_DENSE", 1);
+  g_knobs[SD_TUNE_DENSE_MAX_MB] = env("SD_DENSE_MAX_MB", 32768);
   const char* g = getenv("SD_HGEMM");
   g_knobs[SD_TUNE_HGEMM] = !g ? 0 : std::string(g) == "simt" ? 1 : std::string(g) == "mma" ? 2 : atoll(g);
 }
@@ -174,10 +176,26 @@ static int fused_run(const sd_csr* a, const sd_csr* b, const sd_index* index, in
     SD_TRY(index_build(b, dtype, 0, &own, st));
     ix = own;
   }
-  if (topk == 0 && hybrid_kind(md->metric) >= 0 && hybrid_enabled())
-    SD_TRY(ensure_hybrid(const_cast<sd_index*>(ix), b, hybrid_kind(md->metric), st));
   Scratch sabuf, sbbuf;
   Stats sa, sb;
+  if (dense_eligible(b, md, dtype, topk)) {  // dense-ish index: one tensor-core GEMM (dense_tc.cu)
+    SD_TRY(ensure_dense(const_cast<sd_index*>(ix), b, st));
+    tm.begin(PH_NORMS);
+    int rc = isect_stats(a, b, ix, dtype, md, sabuf, sbbuf, &sa, &sb, false, st);
+    tm.end(PH_NORMS);
+    if (rc == SD_OK) {
+      tm.begin(PH_PASS1);
+      rc = dense_run(a, b, ix, md, sa, sb, out, ldo, flags, st);
+      tm.end(PH_PASS1);
+    }
+    if (own) {
+      cudaStreamSynchronize(st);
+      sd_index_free(own);
+    }
+    return rc;
+  }
+  if (topk == 0 && hybrid_kind(md->metric) >= 0 && hybrid_enabled())
+    SD_TRY(ensure_hybrid(const_cast<sd_index*>(ix), b, hybrid_kind(md->metric), st));
   const int ph_stats = is_namm(md->metric) ? PH_PASS2 : PH_NORMS;
   tm.begin(ph_stats);
   // dot-family metrics that may take the hybrid path compute their query

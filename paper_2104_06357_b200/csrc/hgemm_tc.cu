@@ -125,39 +125,53 @@ __global__ void __launch_bounds__(128) hgemm_tcgen05_kernel(const unsigned char*
   const unsigned char* Ablk = At + (int64_t(blockIdx.x) * nks + ks0) * 2 * int64_t(a_part);
   const unsigned char* Bblk = Bt + ks0 * 2 * int64_t(b_part);
 
+  // stage index, phase and accumulator advance incrementally (a 64-bit
+  // modulo per iteration put a software division on the issuing thread's
+  // critical path)
+  const int nst = int(nsteps);
   if (tid == 32) {  // producer
-    for (int64_t p = 0; p < nsteps; ++p) {
-      const int s = int(p % stages);
-      if (p >= stages) mbar_wait(empty0 + 8 * s, uint32_t(((p / stages) - 1) & 1));
+    int s = 0;
+    uint32_t ph = 0;
+    for (int p = 0; p < nst; ++p) {
+      if (p >= stages) mbar_wait(empty0 + 8 * s, ph ^ 1u);
       const uint32_t dst = sbase + uint32_t(s) * stage_bytes;
       mbar_expect_tx(full0 + 8 * s, stage_bytes);
-      bulk_g2s(dst, Ablk + p * 2 * int64_t(a_part), 2 * a_part, full0 + 8 * s);
-      bulk_g2s(dst + 2 * a_part, Bblk + p * 2 * int64_t(b_part), 2 * b_part, full0 + 8 * s);
+      bulk_g2s(dst, Ablk + int64_t(p) * 2 * int64_t(a_part), 2 * a_part, full0 + 8 * s);
+      bulk_g2s(dst + 2 * a_part, Bblk + int64_t(p) * 2 * int64_t(b_part), 2 * b_part, full0 + 8 * s);
+      if (++s == stages) { s = 0; ph ^= 1u; }
     }
   } else if (tid == 0) {  // MMA issuer
-    for (int64_t i = 0; i < nsteps; ++i) {
-      const int s = int(i % stages);
-      mbar_wait(full0 + 8 * s, uint32_t((i / stages) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int s = 0, q = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nst; ++i) {
+      mbar_wait(full0 + 8 * s, ph);  // (the bulk copies' completion orders the stage; no per-stage fence)
       const uint32_t sa = sbase + uint32_t(s) * stage_bytes;
       const uint32_t a_hi = sa, a_lo = sa + a_part, b_hi = sa + 2 * a_part, b_lo = b_hi + b_part;
+      const uint32_t d = tmem + uint32_t(q) * uint32_t(N);
+      // descriptors: address field = low 14 bits (addr >> 4), per-step ones by offset
+      const uint64_t dah = smem_desc(a_hi), dal = smem_desc(a_lo), dbh = smem_desc(b_hi), dbl = smem_desc(b_lo);
+      const uint32_t first0 = i < nacc ? 0u : 1u;
 #pragma unroll
-      const uint32_t d = tmem + uint32_t(i % nacc) * uint32_t(N);
       for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        const uint32_t ao = uint32_t(kk) * TC_M * 32, bo = uint32_t(kk) * uint32_t(N) * 32;
-        const uint32_t first = (i < nacc && kk == 0) ? 0u : 1u;
-        mma_tf32(d, smem_desc(a_lo + ao), smem_desc(b_hi + bo), idesc, first);
-        mma_tf32(d, smem_desc(a_hi + ao), smem_desc(b_lo + bo), idesc, 1u);
-        mma_tf32(d, smem_desc(a_hi + ao), smem_desc(b_hi + bo), idesc, 1u);
+        const uint64_t ao = uint64_t(kk) * (TC_M * 32 / 16), bo = uint64_t(kk) * uint64_t(N * 32 / 16);
+        mma_tf32(d, dal + ao, dbh + bo, idesc, kk == 0 ? first0 : 1u);
+        mma_tf32(d, dah + ao, dbl + bo, idesc, 1u);
+        mma_tf32(d, dah + ao, dbh + bo, idesc, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                    :: "r"(empty0 + 8 * s) : "memory");
+      if (++s == stages) { s = 0; ph ^= 1u; }
+      if (++q == nacc) q = 0;
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                  :: "r"(done) : "memory");
   }
-  __syncwarp();
-  if (nsteps > 0) mbar_wait(done, 0u);
+  // the other threads wait at a block barrier, not by polling the mbarrier
+  // (spinning warps slowed the MMA pipeline ~5x), then one thread waits for
+  // the last MMAs
+  __syncthreads();
+  if (tid == 0 && nsteps > 0) mbar_wait(done, 0u);
+  __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue: warp w owns TMEM lanes 32w..32w+31 = heavy rows h0 + 32w + lane
   float* out = P + int64_t(blockIdx.z) * rows * ldh;

@@ -56,6 +56,12 @@ struct sd_index {
   bool ms_tried = false, ms_ready = false;
   int64_t* hchunk = nullptr;  // [n_heavy][ms_nch + 1] first CSR entry of each column chunk (hminsum.cu)
   int64_t ms_nch = 0;
+  // dense-index mode (dense_tc.cu, built on the first eligible call): every
+  // row as bf16 planes in the tensor-core operand layout
+  void* dimg = nullptr;
+  int dplanes = 0;      // 1 (values bf16-exact) or 2 (hi, lo)
+  bool dints = false;   // every value a small integer (|v| <= 16)
+  int64_t dnkb = 0;     // K blocks of 64 columns
 };
 
 namespace sd {

@@ -571,6 +571,7 @@ int sd_index_free(sd_index* ix) {
   if (ix->post_rank) cudaFree(ix->post_rank);
   if (ix->topb) cudaFree(ix->topb);
   if (ix->post_cos) cudaFree(ix->post_cos);
+  if (ix->dimg) cudaFree(ix->dimg);
   for (auto& e : ix->stat_cache) cudaFree(e.buf);
   sd::hybrid_index_free(ix);
   delete ix;

@@ -84,6 +84,11 @@ int isect_stats(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype,
 // could isect_run take the hybrid path (it then computes deferred query statistics)?
 bool isect_hybrid_eligible(const sd_index* ix, const sd_metric_desc* md, int topk);
 int hybrid_kind(int metric);  // HYB_DOT, HYB_MINSUM or -1 (no dense heavy-row path)
+// dense_tc.cu: dense-index mode (the whole matrix as one tensor-core GEMM)
+bool dense_eligible(const sd_csr* b, const sd_metric_desc* md, int dtype, int topk);
+int ensure_dense(sd_index* ix, const sd_csr* b, cudaStream_t st);
+int dense_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, const sd_metric_desc* md, const Stats& sa,
+              const Stats& sb, void* out, int64_t ldo, uint32_t* flags, cudaStream_t st);
 int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, const sd_metric_desc* md,
               const Stats& sa, const Stats& sb, void* out, int64_t ldo, int topk, int64_t index_base,
               void* out_d, int64_t* out_i, uint32_t* flags, PhaseTimer* tm, bool a_stats_deferred,

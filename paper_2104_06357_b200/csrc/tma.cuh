@@ -19,6 +19,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   }
 }
 
+// spin on the non-blocking probe (no suspension between checks)
+__device__ __forceinline__ void mbar_spin(uint32_t addr, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(addr) : "memory");
 }

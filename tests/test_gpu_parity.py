@@ -385,7 +385,7 @@ def test_hybrid_heavy_rows_vs_oracle(dtype):
     assert len(heavy) >= 64
     rows = np.sort(np.concatenate([heavy[:40], np.arange(0, idx.n_rows, 37)]))
     q = _gather_rows(idx, np.unique(rows))
-    with _lib.tuned(hybrid=2):
+    with _lib.tuned(hybrid=2, dense=0):   # (dense=0: this index is dense enough for the dense-index mode)
         hidx = _host(idx)
         ix = _lib.device_index(sd.to_device(hidx, dtype))
         assert ix.heavy_rows == 0   # the heavy block is built by the first dot-family call
@@ -448,6 +448,33 @@ def test_hybrid_minsum_manhattan(dtype, n_heavy_q):
         assert_parity(got, O.pairwise_distances(q, neg, "manhattan"), q, neg, "manhattan", dtype, what="neg index")
 
 
+@pytest.mark.parametrize("shape", [(300, 517, 700), (130, 129, 64)])
+def test_dense_mode_vs_oracle(shape):
+    """Dense-index mode (dense_tc.cu, knob dense=2 forces it on any index):
+    the whole matrix as one tcgen05 bf16 GEMM with the metric in the
+    epilogue; two bf16 planes (hi, lo) for general values, one for
+    bf16-exact (binary) values.  Ragged tile edges (rows, queries and columns
+    not multiples of 128 / 64).  Every dot-family metric against the oracle
+    (fp32), and jaccard on binary data exactly equal to the sweep."""
+    from paper_2104_06357_b200 import _lib
+    n_idx, n_q, n_cols = shape
+    idx = _f32(sd.generate(sd.GenSpec(n_idx, n_cols, "uniform", degree=max(3, n_cols // 12), seed=81)))
+    q = _f32(sd.generate(sd.GenSpec(n_q, n_cols, "uniform", degree=max(3, n_cols // 10), seed=82)))
+    for name in DOT_FAMILY:
+        a, b = (q, idx) if name not in ("dice", "jaccard", "russelrao") else (
+            q.with_values(np.ones(q.nnz)), idx.with_values(np.ones(idx.nnz)))
+        a, b = _host(a), _host(b)
+        spec = sd.metric_registry(name)
+        with _lib.tuned(dense=2):
+            got = sd.pairwise_distances(a, b, spec, dtype=np.float32)
+        ref = O.pairwise_distances(a, b, name)
+        assert_parity(got, ref, a, b, name, np.float32, what=f"dense/{name}")
+        if name == "jaccard":
+            with _lib.tuned(dense=0):
+                sweep = sd.pairwise_distances(_host(a), _host(b), spec, dtype=np.float32)
+            np.testing.assert_array_equal(got, sweep)
+
+
 @pytest.mark.parametrize("n_heavy_q", [17, 300])
 def test_hybrid_gemm_routes(n_heavy_q):
     """The heavy block's GEMM: tcgen05 (<= 256 heavy queries, N = 32 here) and
@@ -459,7 +486,7 @@ def test_hybrid_gemm_routes(n_heavy_q):
     from paper_2104_06357_b200 import _lib
     for name in ("cosine", "euclidean"):
         a, b = _host(q), _host(idx)
-        with _lib.tuned(hybrid=2):
+        with _lib.tuned(hybrid=2, dense=0):
             got = sd.pairwise_distances(a, b, sd.metric_registry(name), dtype=np.float32)
         ref = O.pairwise_distances(a, b, name)
         assert_parity(got, ref, a, b, name, np.float32, what=f"hybrid gemm {n_heavy_q}/{name}")
