@@ -201,6 +201,14 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_tensor_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst cuBLAS)"
+    except (OSError, KeyError, ValueError):
+        return 1590.0, "fallback (B200_PROFILING.md)"
+
+
 def load_traffic(workload, metric, dtype):
     """Per-launch DRAM bytes of the sweep kernel from the committed ncu capture
     of the same workload / metric / dtype (profiles/ncu_traffic.json)."""
@@ -476,12 +484,34 @@ def run_ours(args):
             step(metric, tdt, phases)
             kern_ms.append(phases[1])
         kern = statistics.median(kern_ms)
+        if "dense" in ix.hybrid_blocks:
+            # dense-index mode (dense_tc.cu): one tcgen05 bf16 GEMM; tensor-bound.
+            # FLOPs executed = 2 m n K' x the MMAs per K step (hi*hi [+ hi*lo]
+            # [+ lo*hi]), K' = n_cols rounded to 64; `kernel_ms` includes the
+            # query image build (phase pass1)
+            qv = np.asarray(operands_for(metric, index, queries)[1].values, dtype=np.float32)
+            pb = 1 if not (qv.view(np.uint32) & 0xFFFF).any() else 2
+            pa = 2 if "dense_two_planes" in ix.hybrid_blocks else 1
+            terms = 1 + (pb == 2) + (pa == 2)
+            kp = -(-index.n_cols // 64) * 64
+            flops = 2.0 * m * n * kp * terms
+            tpeak, tpeak_kind = load_tensor_peak()
+            achieved = flops / (kern / 1e3) / 1e12
+            path_bytes = compulsory_bytes(m, n, es, dq.nnz, m, di, ix, index.n_cols)
+            return {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": achieved / tpeak, "traffic": None,
+                    "kernel": f"dense_tc_kernel<{metric}> (bf16 {'hi/lo ' if terms > 1 else ''}x{terms})",
+                    "kernel_ms": kern, "flops_per_launch": flops, "mma_terms": terms, "peak_source": tpeak_kind,
+                    "path": {"what": "whole timed step, HBM view: output + operands", "ms": step_ms,
+                             "alg_bytes": path_bytes, "achieved": path_bytes / (step_ms / 1e3) / 1e9,
+                             "frac": path_bytes / (step_ms / 1e3) / 1e9 / peak}}
         # query rows the dense heavy-row path serves instead of the sweep
         deg = np.diff(np.asarray(queries.indptr))
         theta = max(64, (index.n_cols + 31) // 32)
         n_tiles = -(-n // ix.tile_rows)
-        heavy_q = (min(1024, int((deg >= theta).sum())) if ix.heavy_rows > 0 and n_tiles >= 4
-                   and metric in DOT_FAMILY else 0)
+        blocks = ix.hybrid_blocks
+        hybrid = ("dot" in blocks and metric in DOT_FAMILY) or ("minsum" in blocks and metric == "manhattan")
+        heavy_q = min(1024, int((deg >= theta).sum())) if ix.heavy_rows > 0 and n_tiles >= 4 and hybrid else 0
         alg = compulsory_bytes(m - heavy_q, n, es, dq.nnz, m, di, ix, index.n_cols)
         achieved = alg / (kern / 1e3) / 1e9
         path_bytes = compulsory_bytes(m, n, es, dq.nnz, m, di, ix, index.n_cols)

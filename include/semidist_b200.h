@@ -203,9 +203,12 @@ SD_API int sd_index_tile_rows(const sd_index* index);
 /* Index rows held densely for the hybrid path (heavy query rows of dot-family
  * metrics, hybrid.cu); 0 when the index has no heavy-row block. */
 SD_API int64_t sd_index_heavy_rows(const sd_index* index);
-/* Dense heavy-row blocks built so far: bit 0 the dot family's (HT + tensor-core
- * operand image), bit 1 manhattan's min-sum chunk pointers (hminsum.cu; only
- * for an index without negative values).  Same reference role as above. */
+/* Dense blocks built so far: bit 0 the dot family's heavy-row block (HT +
+ * tensor-core operand image), bit 1 manhattan's min-sum chunk pointers
+ * (hminsum.cu; only for an index without negative values), bit 2 the
+ * dense-index image (dense_tc.cu), bit 3 set when that image holds two bf16
+ * planes (hi, lo), bit 4 when every index value is a small integer.  Same
+ * reference role as above. */
 SD_API int sd_index_hybrid_blocks(const sd_index* index);
 
 /* Full distance matrix for one catalog metric (pairwise_distances,

@@ -289,9 +289,12 @@ class DeviceIndex:
 
     @property
     def hybrid_blocks(self):
-        """Dense heavy-row blocks built so far: {"dot", "minsum"} subset."""
+        """Dense blocks built so far: subset of {"dot", "minsum"} (hybrid
+        heavy-row blocks) and {"dense", "dense_two_planes", "dense_ints"}
+        (dense-index mode image)."""
         bits = int(load().sd_index_hybrid_blocks(self.handle))
-        return {n for b, n in ((1, "dot"), (2, "minsum")) if bits & b}
+        return {n for b, n in ((1, "dot"), (2, "minsum"), (4, "dense"), (8, "dense_two_planes"),
+                               (16, "dense_ints")) if bits & b}
 
     def __del__(self):
         try:

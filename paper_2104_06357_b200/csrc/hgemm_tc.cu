@@ -2,8 +2,8 @@
 // tensor cores: D[h][q] = sum_k HT[k][h] * HQT[k][q] for a 128-row tile of
 // heavy index rows (M) and all heavy queries (N <= 256), fp32 via 3xTF32.
 //
-//   * operands live in global memory already in the canonical K-major,
-//     no-swizzle UMMA layout (8-row x 16-byte core matrices), split into tf32
+//   * operands live in global memory already in the K-major 128-byte-swizzled
+//     UMMA layout (one 128-byte line of 32 tf32 per row), split into tf32
 //     hi = tf32(x) and lo = tf32(x - hi), one contiguous block per (row tile,
 //     32-column K-step) (tiled_operand: the index side once per index, the
 //     query side per call), so a stage is two bulk copies (cp.async.bulk,
@@ -33,17 +33,20 @@ __device__ __forceinline__ uint32_t tf32_bits(float x) {
   return r;
 }
 
-// byte offset of element (row r, k in [0, 32)) inside one operand block of
-// R rows: K-step s = k / 8 is its own canonical block of R x 8 tf32
-__device__ __forceinline__ uint32_t kmajor_off(int r, int k, int R) {
-  return uint32_t((k >> 3) * R * 32 + (r >> 3) * 256 + ((k >> 2) & 1) * 128 + (r & 7) * 16 + (k & 3) * 4);
+// byte offset of element (row r, k in [0, 32)) inside one operand block:
+// rows at 128 B, the row's eight 16-byte chunks permuted by chunk ^ (row % 8)
+// (128-byte swizzle: the tensor core's 8-row reads hit every bank; the
+// unswizzled canonical layout left the MMAs at a third of their rate)
+__device__ __forceinline__ uint32_t kmajor_off(int r, int k, int /*R*/) {
+  return uint32_t(r * 128 + ((((k * 4) >> 4) ^ (r & 7)) << 4) + ((k * 4) & 15));
 }
 
-// shared-memory matrix descriptor: K-major, no swizzle, LBO = 128 B (the
-// second 16-byte K chunk), SBO = 256 B (next 8 rows), version 1 (sm_100)
+// shared-memory matrix descriptor: K-major, SWIZZLE_128B (layout type 2),
+// SBO = 1024 B (next 8 rows), LBO unused, version 1 (sm_100); the K = 8 step
+// kk starts 32 B further into the 1024-byte aligned block
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
-         (uint64_t(1) << 46);
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(128) hgemm_tcgen05_kernel(const unsigned char*
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t a_part = TC_M * TC_BK * 4, b_part = uint32_t(N) * TC_BK * 4;
   const uint32_t stage_bytes = 2 * a_part + 2 * b_part;
-  const uint32_t sbase = uint32_t(__cvta_generic_to_shared(smem));
+  const uint32_t sbase = (uint32_t(__cvta_generic_to_shared(smem)) + 1023u) & ~1023u;  // 1 KB slack allocated
   __shared__ __align__(8) unsigned long long bars[2 * 8 + 1];  // full[8], empty[8], done
   __shared__ uint32_t tmem_slot;
   const uint32_t full0 = uint32_t(__cvta_generic_to_shared(&bars[0])), empty0 = full0 + 64, done = full0 + 128;
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(128) hgemm_tcgen05_kernel(const unsigned char*
       const uint32_t first0 = i < nacc ? 0u : 1u;
 #pragma unroll
       for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        const uint64_t ao = uint64_t(kk) * (TC_M * 32 / 16), bo = uint64_t(kk) * uint64_t(N * 32 / 16);
+        const uint64_t ao = uint64_t(kk) * 2, bo = uint64_t(kk) * 2;  // 32 B per K = 8 step
         mma_tf32(d, dal + ao, dbh + bo, idesc, kk == 0 ? first0 : 1u);
         mma_tf32(d, dah + ao, dbl + bo, idesc, 1u);
         mma_tf32(d, dah + ao, dbh + bo, idesc, 1u);
@@ -217,8 +220,8 @@ int tiled_operand(const sd_csr* m, const int32_t* rows, int64_t nrows, int R, in
 int hgemm_tcgen05(const void* at, const void* bt, int64_t nks, int64_t hpad, int N, int64_t per, int64_t rows,
                   float* part, cudaStream_t st) {
   const size_t stage = 2 * size_t(TC_M) * TC_BK * 4 + 2 * size_t(N) * TC_BK * 4;
-  const int stages = int(std::min<int64_t>(8, std::max<int64_t>(2, (smem_optin_bytes() - 2048) / int64_t(stage))));
-  const size_t smem = size_t(stages) * stage;
+  const int stages = int(std::min<int64_t>(8, std::max<int64_t>(2, (smem_optin_bytes() - 4096) / int64_t(stage))));
+  const size_t smem = size_t(stages) * stage + 1024;
   SD_TRY(prepare_smem(hgemm_tcgen05_kernel, smem, "hgemm_tcgen05_kernel"));
   const dim3 grid{unsigned(hpad / TC_M), 1u, unsigned((nks + per - 1) / per)};
   hgemm_tcgen05_kernel<<<grid, 128, smem, st>>>(static_cast<const unsigned char*>(at),

@@ -581,4 +581,8 @@ int sd_index_free(sd_index* ix) {
 int64_t sd_index_bytes(const sd_index* ix) { return ix ? ix->bytes : 0; }
 int sd_index_tile_rows(const sd_index* ix) { return ix ? ix->tile : 0; }
 int64_t sd_index_heavy_rows(const sd_index* ix) { return ix ? ix->n_heavy : 0; }
-int sd_index_hybrid_blocks(const sd_index* ix) { return ix ? (ix->dot_ready ? 1 : 0) | (ix->ms_ready ? 2 : 0) : 0; }
+int sd_index_hybrid_blocks(const sd_index* ix) {
+  if (!ix) return 0;
+  return (ix->dot_ready ? 1 : 0) | (ix->ms_ready ? 2 : 0) | (ix->dimg ? 4 : 0) | (ix->dplanes == 2 ? 8 : 0) |
+         (ix->dimg && ix->dints ? 16 : 0);
+}
