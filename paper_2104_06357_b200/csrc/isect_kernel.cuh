@@ -677,21 +677,20 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
     for (int v0 = threadIdx.x; v0 < nv; v0 += int(blockDim.x) * SU) {
       T r[SU][4];
 #pragma unroll
-      for (int u = 0; u < SU; ++u) {
+      for (int u = 0; u < SU; ++u) {  // (heavy index rows have no dlh row: never read)
         const int v = v0 + u * int(blockDim.x);
-        if (v < nv) V4<T>::load(dlh + j0 * qpad + 4 * int64_t(v), r[u]);
+        if (v < nv && __ldg(hid + j0 + v / qv) < 0) V4<T>::load(dlh + j0 * qpad + 4 * int64_t(v), r[u]);
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         const int v = v0 + u * int(blockDim.x);
-        if (v < nv) {
+        if (v < nv && __ldg(hid + j0 + v / qv) < 0) {
           const int jj = v / qv, q = 4 * (v - jj * qv);
 #pragma unroll
           for (int t = 0; t < 4; ++t) sv[jj * qs + q + t] = r[u][t];
         }
       }
     }
-    __syncthreads();  // the dense-block rows below overwrite what the loop above staged for them
     // heavy index rows of the block (no dlh row): their sums from the dense
     // block, split over the warps by ordinal
     {

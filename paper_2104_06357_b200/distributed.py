@@ -76,11 +76,15 @@ def gather_candidates(dist_t, idx_t, group=None):
         dist.all_gather_into_tensor(out_d, dist_t.contiguous(), group=group)
         dist.all_gather_into_tensor(out_i, idx_t.contiguous(), group=group)
         return out_d, out_i
-    parts_d = [torch.empty_like(dist_t) for _ in range(world)]
-    parts_i = [torch.empty_like(idx_t) for _ in range(world)]
-    dist.all_gather(parts_d, dist_t.contiguous(), group=group)
-    dist.all_gather(parts_i, idx_t.contiguous(), group=group)
-    return torch.stack(parts_d), torch.stack(parts_i)
+    # gloo (CPU tests, or several ranks sharing one GPU): stage device
+    # candidates through host memory, return them on the caller's device
+    dev = dist_t.device
+    hd, hi = dist_t.detach().to("cpu").contiguous(), idx_t.detach().to("cpu").contiguous()
+    parts_d = [torch.empty_like(hd) for _ in range(world)]
+    parts_i = [torch.empty_like(hi) for _ in range(world)]
+    dist.all_gather(parts_d, hd, group=group)
+    dist.all_gather(parts_i, hi, group=group)
+    return torch.stack(parts_d).to(dev), torch.stack(parts_i).to(dev)
 
 
 def merge_candidates(cand_d, cand_i, k):
