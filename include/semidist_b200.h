@@ -153,7 +153,10 @@ typedef enum {
   SD_TUNE_HGEMM = 10,          /* SD_HGEMM: 0 automatic, 1 CUDA-core, 2 mma.sync */
   SD_TUNE_DENSE = 11,          /* SD_DENSE: dense-index tensor-core mode, 0 off, 1 automatic, 2 forced */
   SD_TUNE_DENSE_MAX_MB = 12,   /* SD_DENSE_MAX_MB: largest dense index image (MiB) */
-  SD_TUNE_COUNT = 13
+  SD_TUNE_GATHER_SHADOW = 13,  /* SD_GATHER_SHADOW (experiment): 1 = hybrid gather co-resident with the sweep
+                                  (one 128-thread block per SM, sweep capped at 12 warps); default 0 = gather on
+                                  every SM first (C2 cosine 1.98 ms vs 3.66 ms co-resident) */
+  SD_TUNE_COUNT = 14
 } sd_tune_knob;
 
 /* ---------------------------------------------------------------- misc */

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsemidist_b200.so")
-SOURCES = ["api.cu", "prep.cu", "engine.cu", "epilogue.cu", "isect.cu", "isect_f32.cu", "isect_f64.cu", "topk.cu", "hybrid.cu", "hgemm_tc.cu", "hminsum.cu", "dense_tc.cu", "util.cu"]
+SOURCES = ["api.cu", "prep.cu", "engine.cu", "epilogue.cu", "isect.cu", "isect_f32.cu", "isect_f64.cu", "topk.cu", "hybrid.cu", "hminsum.cu", "dense_tc.cu", "util.cu"]
 HEADERS = ["common.cuh", "semiring.cuh", "metric.cuh", "prep.cuh", "topk.cuh", "isect_kernel.cuh", "index.cuh", "hybrid.cuh", "tma.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

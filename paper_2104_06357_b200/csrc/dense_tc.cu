@@ -74,14 +74,15 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
 // rows of a CSR into the image: [row tile of R][K block][plane][R x 128 B];
 // the (rows x chunks) grid of the other scatter kernels
 __global__ void dense_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                                     const float* __restrict__ val, int64_t nrows, int64_t nkb, int planes, int R,
-                                     unsigned char* __restrict__ img) {
+                                     const float* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                                     int64_t nkb, int planes, int R, unsigned char* __restrict__ img) {
   const int64_t plane = int64_t(R) * DT_KB * 2;
   for (int64_t g = blockIdx.x; g < nrows; g += gridDim.x) {
     const int64_t tile = g / R;
     const int rr = int(g - tile * R);
+    const int64_t src = rows ? int64_t(rows[g]) : g;  // image row g = CSR row src
     const int64_t step = int64_t(gridDim.y) * blockDim.x;
-    for (int64_t e = ptr[g] + int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < ptr[g + 1]; e += step) {
+    for (int64_t e = ptr[src] + int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < ptr[src + 1]; e += step) {
       const int64_t k = idx[e];
       const float v = val[e];
       const __nv_bfloat16 hi = __float2bfloat16_rn(v);
@@ -118,10 +119,14 @@ struct DenseArgs {
   float k, p;
   float* out;
   uint32_t* flags;
+  // RAW (the hybrid path's heavy block): K blocks [z*per, (z+1)*per) per
+  // blockIdx.z, raw sums to part[z][q][h] (q < prow, h < ldp; zero padding included)
+  int64_t per, prow, ldp;
+  float* part;
 };
 
 // N queries per CTA (128, or 256 for one-plane operands): 512 / N accumulators
-template <int M, int N>
+template <int M, int N, bool RAW>
 __global__ void __launch_bounds__(128, 1) dense_tc_kernel(const DenseArgs a, int stages) {
   constexpr int NACC = 512 / N;
   constexpr uint32_t BPLANE = uint32_t(N) * DT_KB * 2u;
@@ -159,12 +164,13 @@ __global__ void __launch_bounds__(128, 1) dense_tc_kernel(const DenseArgs a, int
   // instruction descriptor: D f32, A/B bf16, both K-major, N >> 3, M >> 4
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(DT_M >> 4) << 24);
   const int64_t qt = blockIdx.x, jt = blockIdx.y;
-  const unsigned char* Ablk = a.ai + jt * a.nkb * int64_t(a_bytes);
-  const unsigned char* Bblk = a.bq + qt * a.nkb * int64_t(2 * BPLANE);
+  const int64_t kb0 = RAW ? int64_t(blockIdx.z) * a.per : 0;
+  const unsigned char* Ablk = a.ai + (jt * a.nkb + kb0) * int64_t(a_bytes);
+  const unsigned char* Bblk = a.bq + (qt * a.nkb + kb0) * int64_t(2 * BPLANE);
   // stage index and barrier phase advance incrementally: a 64-bit `p % stages`
   // per iteration (a software division on one thread's dependent chain)
   // cost ~0.4 us per stage, more than the MMAs themselves
-  const int nkb = int(a.nkb);
+  const int nkb = int(RAW ? tmin<int64_t>(a.per, a.nkb - kb0) : a.nkb);
   if (tid == 32) {  // producer
     int s = 0;
     uint32_t ph = 0;
@@ -217,14 +223,14 @@ __global__ void __launch_bounds__(128, 1) dense_tc_kernel(const DenseArgs a, int
   // (spinning warps slowed the MMA pipeline ~5x), then one thread waits for
   // the last MMAs
   __syncthreads();
-  if (tid == 0 && a.nkb > 0) mbar_wait(done, 0u);
+  if (tid == 0 && nkb > 0) mbar_wait(done, 0u);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue: warp w owns TMEM lanes 32w..32w+31 = index rows j
   const int64_t j = jt * DT_M + warp * 32 + lane;
   const bool jok = j < a.n;
   const float gb0 = jok && a.sb0 ? a.sb0[j] : 0.f, gb1 = jok && a.sb1 ? a.sb1[j] : 0.f;
-  const int used = int(tmin<int64_t>(NACC, a.nkb));
+  const int used = int(tmin<int64_t>(NACC, nkb));
   uint32_t flags = 0;
   for (int c0 = 0; c0 < N; c0 += 16) {
     float sum[16];
@@ -241,6 +247,14 @@ __global__ void __launch_bounds__(128, 1) dense_tc_kernel(const DenseArgs a, int
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int c = 0; c < 16; ++c) sum[c] = __fadd_rn(sum[c], __uint_as_float(r[c]));
+    }
+    if constexpr (RAW) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int64_t q = qt * N + c0 + c;
+        if (q < a.prow && j < a.ldp) a.part[(int64_t(blockIdx.z) * a.prow + q) * a.ldp + j] = sum[c];
+      }
+      continue;
     }
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
@@ -261,16 +275,16 @@ __global__ void __launch_bounds__(128, 1) dense_tc_kernel(const DenseArgs a, int
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(NCOLS) : "memory");
 }
 
-template <int M, int N>
-int launch_dense_n(const DenseArgs& a, cudaStream_t st) {
+template <int M, int N, bool RAW = false>
+int launch_dense_n(const DenseArgs& a, cudaStream_t st, unsigned splits = 1) {
   // as many stages as fit: the stages stream from the L2, whose latency the
   // pipeline depth hides
   const size_t stage = size_t(a.pa) * DT_PLANE + size_t(a.pb) * size_t(N) * DT_KB * 2;
   const int stages = int(std::min<int64_t>(DT_MAX_STAGES, (smem_optin_bytes() - 6144) / int64_t(stage)));
   const size_t smem = size_t(stages) * stage + 1024;
-  SD_TRY(prepare_smem(dense_tc_kernel<M, N>, smem, "dense_tc_kernel"));
-  const dim3 grid{unsigned((a.m + N - 1) / N), unsigned((a.n + DT_M - 1) / DT_M), 1u};
-  dense_tc_kernel<M, N><<<grid, 128, smem, st>>>(a, stages);
+  SD_TRY(prepare_smem(dense_tc_kernel<M, N, RAW>, smem, "dense_tc_kernel"));
+  const dim3 grid{unsigned((a.m + N - 1) / N), unsigned((a.n + DT_M - 1) / DT_M), splits};
+  dense_tc_kernel<M, N, RAW><<<grid, 128, smem, st>>>(a, stages);
   SD_LAUNCH_CHECK();
   return SD_OK;
 }
@@ -288,6 +302,8 @@ int launch_dense(const DenseArgs& a, int N, cudaStream_t st) {
   return N == 256 ? launch_dense_n<M, 256>(a, st) : launch_dense_n<M, 128>(a, st);
 }
 
+}  // namespace
+
 int check_bf16_exact(const sd_csr* m, unsigned int* flag, cudaStream_t st) {
   if (m->nnz == 0) return SD_OK;
   const int blocks = int(tmin<int64_t>((m->nnz + 255) / 256, int64_t(num_sms()) * 8));
@@ -296,16 +312,19 @@ int check_bf16_exact(const sd_csr* m, unsigned int* flag, cudaStream_t st) {
   return SD_OK;
 }
 
+namespace {
+
 size_t image_bytes(int64_t rows, int64_t nkb, int planes, int R) {
   return size_t((rows + R - 1) / R) * size_t(nkb) * size_t(planes) * size_t(R) * DT_KB * 2;
 }
 
-int build_image(const sd_csr* m, int64_t nkb, int planes, int R, void* img, cudaStream_t st) {
-  SD_CUDA_TRY(cudaMemsetAsync(img, 0, image_bytes(m->n_rows, nkb, planes, R), st));
-  if (m->n_rows == 0 || m->nnz == 0) return SD_OK;
-  dense_scatter_kernel<<<row_scatter_grid(m->n_rows), 256, 0, st>>>(m->indptr, m->indices,
-                                                                  static_cast<const float*>(m->values), m->n_rows,
-                                                                  nkb, planes, R, static_cast<unsigned char*>(img));
+int build_image(const sd_csr* m, const int32_t* rows, int64_t nrows, int64_t nkb, int planes, int R, void* img,
+                cudaStream_t st) {
+  SD_CUDA_TRY(cudaMemsetAsync(img, 0, image_bytes(nrows, nkb, planes, R), st));
+  if (nrows == 0 || m->nnz == 0) return SD_OK;
+  dense_scatter_kernel<<<row_scatter_grid(nrows), 256, 0, st>>>(m->indptr, m->indices,
+                                                               static_cast<const float*>(m->values), rows, nrows,
+                                                               nkb, planes, R, static_cast<unsigned char*>(img));
   SD_LAUNCH_CHECK();
   return SD_OK;
 }
@@ -344,7 +363,7 @@ int ensure_dense(sd_index* ix, const sd_csr* b, cudaStream_t st) {
     set_error("cudaMalloc failed for the dense index image");
     return SD_E_CUDA;
   }
-  const int rc = build_image(b, nkb, planes, DT_M, img, st);
+  const int rc = build_image(b, nullptr, b->n_rows, nkb, planes, DT_M, img, st);
   if (rc != SD_OK) { cudaFree(img); return rc; }
   ix->dimg = img;
   ix->dplanes = planes;
@@ -374,7 +393,7 @@ int dense_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, const sd_met
   const int pb = (inexact & 1u) ? 2 : 1;
   const int R = dense_tile_n(ix->dints && (inexact & 2u) == 0, a->n_cols);
   SD_TRY(img.alloc(image_bytes(a->n_rows, nkb, 2, R), st));
-  SD_TRY(build_image(a, nkb, 2, R, img.ptr, st));
+  SD_TRY(build_image(a, nullptr, a->n_rows, nkb, 2, R, img.ptr, st));
   DenseArgs d;
   d.ai = static_cast<const unsigned char*>(ix->dimg);
   d.bq = static_cast<const unsigned char*>(img.ptr);
@@ -398,6 +417,32 @@ int dense_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, const sd_met
     case SD_M_RUSSELRAO: return launch_dense<SD_M_RUSSELRAO>(d, R, st);
     default: set_error("metric has no dense-index mode"); return SD_E_UNSUPPORTED;
   }
+}
+
+// The hybrid path's heavy block on the same kernel (hybrid.cu): an image of
+// rows `rows` of a CSR (nrows of them, tiles of R) ...
+int64_t dense_kblocks(int64_t n_cols) { return (n_cols + DT_KB - 1) / DT_KB; }
+size_t dense_image_bytes(int64_t nrows, int64_t nkb, int planes, int R) { return image_bytes(nrows, nkb, planes, R); }
+int dense_image(const sd_csr* m, const int32_t* rows, int64_t nrows, int64_t nkb, int planes, int R, void* img,
+                cudaStream_t st) {
+  return build_image(m, rows, nrows, nkb, planes, R, img, st);
+}
+
+// ... and P[z][q][h] = sum over K blocks [z*per, (z+1)*per) of A_h . B_q for
+// the index image A (na rows, pa planes, tiles of 128) and the query image B
+// (nq rows, 2 planes stored, pb used, tiles of N = R), q < prow, h < ldp
+int dense_gemm_raw(const void* aimg, int pa, int64_t na, const void* bimg, int pb, int R, int64_t nq, int64_t nkb,
+                   int64_t per, float* part, int64_t prow, int64_t ldp, cudaStream_t st) {
+  DenseArgs d{};
+  d.ai = static_cast<const unsigned char*>(aimg);
+  d.bq = static_cast<const unsigned char*>(bimg);
+  d.nkb = nkb;
+  d.pa = pa;
+  d.pb = pb;
+  d.m = nq; d.n = na;
+  d.per = per; d.prow = prow; d.ldp = ldp; d.part = part;
+  const unsigned splits = unsigned((nkb + per - 1) / per);
+  return R == 256 ? launch_dense_n<SD_M_DOT, 256, true>(d, st, splits) : launch_dense_n<SD_M_DOT, 128, true>(d, st, splits);
 }
 
 }  // namespace sd

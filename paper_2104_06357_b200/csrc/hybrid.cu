@@ -125,16 +125,25 @@ static int hybrid_dot_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream
     return SD_OK;
   }));
   ix->bytes += dense_bytes;
-  if (dtype == SD_F32) {  // A operand image of the tensor-core GEMM
-    const int64_t nks = (b->n_cols + tc_kstep() - 1) / tc_kstep();
-    const int64_t tbytes = (pad / 128) * nks * 2 * 128 * tc_kstep() * 4;
-    if (cudaMalloc(&ix->ht_tiled, tbytes) != cudaSuccess) {
-      set_error("cudaMalloc failed for the hybrid index (tiled)");
+  if (dtype == SD_F32) {  // the heavy rows as the tcgen05 GEMM's bf16 operand image (dense_tc.cu)
+    Scratch flag;
+    SD_TRY(flag.alloc(sizeof(unsigned int), st));
+    SD_CUDA_TRY(cudaMemsetAsync(flag.ptr, 0, sizeof(unsigned int), st));
+    SD_TRY(check_bf16_exact(b, flag.as<unsigned int>(), st));
+    unsigned int inexact = 0;
+    SD_CUDA_TRY(cudaMemcpyAsync(&inexact, flag.ptr, sizeof(inexact), cudaMemcpyDeviceToHost, st));
+    SD_CUDA_TRY(cudaStreamSynchronize(st));
+    const int planes = (inexact & 1u) ? 2 : 1;
+    const int64_t nkb = dense_kblocks(b->n_cols);
+    const size_t tbytes = dense_image_bytes(nh, nkb, planes, 128);
+    if (cudaMalloc(&ix->hbf, tbytes) != cudaSuccess) {
+      set_error("cudaMalloc failed for the hybrid index (bf16 image)");
       return SD_E_CUDA;
     }
-    SD_TRY(tiled_operand(b, ix->hrows, nh, 128, nks, ix->ht_tiled, st));
-    ix->nks = nks;
-    ix->bytes += tbytes;
+    SD_TRY(dense_image(b, ix->hrows, nh, nkb, planes, 128, ix->hbf, st));
+    ix->hbf_planes = planes;
+    ix->hbf_nkb = nkb;
+    ix->bytes += int64_t(tbytes);
   }
   SD_CUDA_TRY(cudaStreamSynchronize(st));
   ix->dot_ready = true;
@@ -187,11 +196,11 @@ void hybrid_index_free(sd_index* ix) {
   if (ix->hid) cudaFree(ix->hid);
   if (ix->ht) cudaFree(ix->ht);
   if (ix->lrows) cudaFree(ix->lrows);
-  if (ix->ht_tiled) cudaFree(ix->ht_tiled);
+  if (ix->hbf) cudaFree(ix->hbf);
   if (ix->hrows) cudaFree(ix->hrows);
   if (ix->hperm) cudaFree(ix->hperm);
   if (ix->hchunk) cudaFree(ix->hchunk);
-  ix->ht_tiled = nullptr;
+  ix->hbf = nullptr;
   ix->hrows = nullptr;
   ix->hperm = nullptr;
   ix->hchunk = nullptr;
@@ -493,21 +502,69 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
 
 // ---------------------------------------------------------------- driver
 
-int hybrid_classify(const sd_csr* a, const sd_index* ix, HybridState& hs, cudaStream_t st) {
+int hybrid_classify(const sd_csr* a, const sd_index* ix, int dtype, int kind, HybridState& hs, cudaStream_t st) {
   hs.nhq = 0;
   const int64_t m = a->n_rows;
   const int cap = int(std::max<int64_t>(1, knob(SD_TUNE_HYBRID_MAX_QUERIES)));
   SD_TRY(hs.qid.alloc(sizeof(int32_t) * std::max<int64_t>(1, m), st));
   SD_TRY(hs.hq.alloc(sizeof(int32_t) * cap, st));
-  SD_TRY(hs.count.alloc(sizeof(unsigned int), st));
-  SD_CUDA_TRY(cudaMemsetAsync(hs.count.ptr, 0, sizeof(unsigned int), st));
+  SD_TRY(hs.count.alloc(2 * sizeof(unsigned int), st));
+  SD_CUDA_TRY(cudaMemsetAsync(hs.count.ptr, 0, 2 * sizeof(unsigned int), st));
   SD_TRY(hs.gcount.alloc(sizeof(unsigned long long), st));
   SD_CUDA_TRY(cudaMemsetAsync(hs.gcount.ptr, 0, sizeof(unsigned long long), st));
   const int blocks = int(std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 8));
   classify_kernel<<<std::max(1, blocks), 256, 0, st>>>(a->indptr, m, ix->heavy_deg, cap, hs.qid.as<int32_t>(),
                                                        hs.hq.as<int32_t>(), hs.count.as<unsigned int>());
   SD_LAUNCH_CHECK();
+  if (dtype == SD_F32 && kind == HYB_DOT && ix->hbf)  // planes of the queries' GEMM image (read with the count)
+    SD_TRY(check_bf16_exact(a, hs.count.as<unsigned int>() + 1, st));
   hs.cap = cap;
+  return SD_OK;
+}
+
+// The dense gather on side stream 0 (after hs.fork): DLH for the light index
+// rows.  Shadow mode: one 128-thread block per SM next to the sweep's CTAs.
+int hybrid_gather(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, HybridState& hs, cudaStream_t st) {
+  if (hs.nhq == 0) return SD_OK;
+  const bool ms = hs.gather_kind == HYB_MINSUM;
+  const int64_t K = a->n_cols, nblk = hs.qpad / 128;
+  const int64_t hq_bstride = ms ? K * 128 : 128, hq_ld = ms ? 128 : hs.qpad;
+  cudaStream_t side = hs.fork ? side_stream(0) : st;
+  if (side != st) SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
+  // keep the SMs' shared-memory carveout at its maximum while the gather
+  // runs, so CTAs needing ~200 KB of shared memory can co-reside with it
+  static const bool carve = [] {
+    cudaFuncSetAttribute(hgather_kernel<float, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<float, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<double, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<double, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)carve;
+  const bool shadow = knob(SD_TUNE_GATHER_SHADOW) != 0;
+  const int gthreads = shadow ? 128 : 256;
+  SD_TRY(SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
+    int per_sm = 0;
+    if (ms) {
+      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, true>, 256, 0));
+      if (shadow) per_sm = 1;
+      hgather_kernel<T, true><<<std::max(1, per_sm) * num_sms(), gthreads, 0, side>>>(
+          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
+          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+    } else {
+      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, false>, 256, 0));
+      if (shadow) per_sm = 1;
+      hgather_kernel<T, false><<<std::max(1, per_sm) * num_sms(), gthreads, 0, side>>>(
+          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
+          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
+    }
+    SD_LAUNCH_CHECK();
+    return SD_OK;
+  }));
+  if (side != st) {
+    SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
+    SD_CUDA_TRY(cudaEventRecord(hs.join, side));
+  }
   return SD_OK;
 }
 
@@ -515,10 +572,11 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
                    cudaStream_t st) {
   // the host needs the heavy count to size the dense block: one small read
   // (work queued on the side streams before it keeps the GPU busy meanwhile)
-  unsigned int cnt = 0;
-  SD_CUDA_TRY(cudaMemcpyAsync(&cnt, hs.count.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+  unsigned int cnt[2] = {0, 0};
+  SD_CUDA_TRY(cudaMemcpyAsync(cnt, hs.count.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, st));
   SD_CUDA_TRY(cudaStreamSynchronize(st));
-  hs.nhq = int(std::min<unsigned int>(cnt, unsigned(hs.cap)));
+  hs.nhq = int(std::min<unsigned int>(cnt[0], unsigned(hs.cap)));
+  const int q_planes = (cnt[1] & 1u) ? 2 : 1;
   if (hs.nhq == 0) return SD_OK;
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t K = a->n_cols;
@@ -534,45 +592,22 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   const int64_t hq_bstride = ms ? K * 128 : 128, hq_ld = ms ? 128 : hs.qpad;
   // the dense gather runs on a side stream (heavy_rows joins it), after the
   // dense block
-  auto gather = [&](auto tag) -> int {
-    using T = decltype(tag);
-    cudaStream_t side = side_stream(0);
-    if (!side) side = st;
-    if (side != st) {
-      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));
-      SD_CUDA_TRY(cudaEventRecord(hs.fork, st));
-      SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
-    }
-    int per_sm = 0;
-    // keep the SMs' shared-memory carveout at its maximum while the gather
-    // runs, so the dense block's CTAs (~200 KB of stages) co-reside with it
-    // instead of waiting for SMs to drain
-    static const bool carve = [] {
-      cudaFuncSetAttribute(hgather_kernel<float, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(hgather_kernel<float, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(hgather_kernel<double, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(hgather_kernel<double, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      return true;
-    }();
-    (void)carve;
-    if (ms) {
-      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, true>, 256, 0));
-      hgather_kernel<T, true><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
-          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
-          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
-    } else {
-      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, false>, 256, 0));
-      hgather_kernel<T, false><<<std::max(1, per_sm) * num_sms(), 256, 0, side>>>(
-          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
-          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
-    }
-    SD_LAUNCH_CHECK();
-    if (side != st) {
-      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
-      SD_CUDA_TRY(cudaEventRecord(hs.join, side));
-      hs.main = st;
-    }
-    return SD_OK;
+  // the gather forks now (it only needs HQT).  Shadow mode (knob, off by
+  // default) launches it after the sweep (hybrid_gather, from isect_run) with
+  // one 128-thread block per SM beside the sweep's CTAs: measured on C2
+  // cosine it loses (3.66 vs 1.98 ms) — 4 warps per SM leave the
+  // latency-bound gather ~10x slower than alone, and the sweep at 12 warps
+  // 13 % slower
+  cudaStream_t side = side_stream(0);
+  if (side && side != st) {
+    SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.fork, cudaEventDisableTiming));
+    hs.main = st;
+  }
+  hs.gather_kind = kind;
+  auto gather = [&](auto) -> int {
+    if (hs.fork) SD_CUDA_TRY(cudaEventRecord(hs.fork, st));
+    if (knob(SD_TUNE_GATHER_SHADOW) != 0) return SD_OK;  // launched by hybrid_gather after the sweep
+    return hybrid_gather(a, b, ix, dtype, hs, st);
   };
   if (ms) {
     return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
@@ -584,26 +619,28 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
       return hminsum(ix, b, dtype, hs.hqt.ptr, K, hs.qpad, hs.part, hs.dqh.ptr, st);
     });
   }
-  // fp32: tcgen05 3xTF32 GEMM (M = 128 heavy index rows x N = all heavy
-  // queries, hgemm_tc.cu) when they fit one tile (<= 256), else mma.sync
-  // 3xTF32 (tile 32 x 128 x 32); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
+  // fp32: tcgen05 bf16 GEMM (dense_tc.cu; hi/lo planes where values are
+  // not bf16-exact, M = 128 heavy index rows x N = 128 or 256 heavy queries,
+  // K split over ~2 waves of CTAs); mma.sync 3xTF32 (tile 32 x 128 x 32) when
+  // forced; fp64: CUDA-core DFMA (tile 32 x 128 x 16)
   const int64_t ge = knob(SD_TUNE_HGEMM);  // experiment override: 1 CUDA cores, 2 mma.sync
   const bool simt = ge == 1;
-  const bool tc5 = dtype == SD_F32 && ix->ht_tiled && hs.nhq <= 256 && !simt && ge != 2;
-  const bool tc = dtype == SD_F32 && !simt && !tc5;
-  const int64_t bm = tc5 ? (hs.nhq + 15) / 16 * 16 : tc ? TG_BM : HG_BM;
-  const int64_t bn = tc5 ? 128 : tc ? TG_BN : HG_BN, bkk = tc5 ? tc_kstep() : tc ? TG_BK : HG_BK;
+  const bool tcb = dtype == SD_F32 && ix->hbf && !simt && ge != 2;
+  const bool tc = dtype == SD_F32 && !simt && !tcb;
+  const int R = hs.nhq <= 128 ? 128 : 256;  // queries per GEMM CTA
+  const int64_t bm = tcb ? R : tc ? TG_BM : HG_BM;
+  const int64_t bn = tcb ? 128 : tc ? TG_BN : HG_BN, bkk = tcb ? 64 : tc ? TG_BK : HG_BK;
   const int64_t tiles_q = (hs.nhq + bm - 1) / bm, tiles_h = ix->hpad / bn;
-  const int64_t rows = tiles_q * bm;  // GEMM rows computed (<= qpad)
+  const int64_t rows = tcb ? hs.qpad : tiles_q * bm;  // GEMM rows written (<= qpad)
   // K split so that the GEMM fills about two (tensor-core) or six waves of CTAs
-  const int64_t waves = tc5 ? 4 : 3 * 2;
+  const int64_t waves = tcb ? 2 : 3 * 2;
   const int64_t want = std::max<int64_t>(1, (waves * int64_t(num_sms()) + tiles_q * tiles_h - 1) / (tiles_q * tiles_h));
   int64_t kchunk = (K + want - 1) / want;
   kchunk = std::max<int64_t>(bkk, (kchunk + bkk - 1) / bkk * bkk);
   const int64_t splits = (K + kchunk - 1) / kchunk;
-  if (tc5) {  // B operand image of this call's heavy queries
-    SD_TRY(hs.hq_tiled.alloc(size_t(ix->nks) * 2 * size_t(bm) * tc_kstep() * 4, st));
-    SD_TRY(tiled_operand(a, hs.hq.as<int32_t>(), hs.nhq, int(bm), ix->nks, hs.hq_tiled.ptr, st));
+  if (tcb) {  // the bf16 image of this call's heavy queries
+    SD_TRY(hs.hq_img.alloc(dense_image_bytes(hs.nhq, ix->hbf_nkb, 2, R), st));
+    SD_TRY(dense_image(a, hs.hq.as<int32_t>(), hs.nhq, ix->hbf_nkb, 2, R, hs.hq_img.ptr, st));
   }
   SD_TRY(hs.part.alloc(es * size_t(splits) * size_t(rows) * size_t(ix->hpad), st));
   return SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
@@ -613,9 +650,9 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     SD_LAUNCH_CHECK();
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
     if constexpr (sizeof(T) == 4) {
-      if (tc5)
-        SD_TRY(hgemm_tcgen05(ix->ht_tiled, hs.hq_tiled.ptr, ix->nks, ix->hpad, int(bm), kchunk / bkk, rows,
-                             hs.part.as<float>(), st));
+      if (tcb)
+        SD_TRY(dense_gemm_raw(ix->hbf, ix->hbf_planes, ix->n_heavy, hs.hq_img.ptr, q_planes, R, hs.nhq,
+                              ix->hbf_nkb, kchunk / bkk, hs.part.as<float>(), rows, ix->hpad, st));
       else if (tc)
         hgemm_tf32x3_kernel<<<grid, 128, 0, st>>>(hs.hqt.as<float>(), static_cast<const float*>(ix->ht), K, hs.qpad,
                                                   ix->hpad, kchunk, ix->hpad, rows, hs.part.as<float>());

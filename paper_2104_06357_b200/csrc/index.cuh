@@ -50,8 +50,9 @@ struct sd_index {
   // dot family (C_MUL)
   bool dot_tried = false, dot_ready = false;
   void* ht = nullptr;      // [n_cols][hpad] T: HT[c][h] = B[heavy row h][c]
-  void* ht_tiled = nullptr;  // fp32: HT as the tensor-core GEMM's A operand image (hgemm_tc.cu)
-  int64_t nks = 0;           // its K-steps of 32 columns
+  void* hbf = nullptr;       // fp32: the heavy rows as the tcgen05 GEMM's bf16 operand image (dense_tc.cu)
+  int hbf_planes = 0;        // 1 (values bf16-exact) or 2 (hi, lo)
+  int64_t hbf_nkb = 0;       // its K blocks of 64 columns
   // min-sum (C_ABS, manhattan; only when every value of B is >= 0)
   bool ms_tried = false, ms_ready = false;
   int64_t* hchunk = nullptr;  // [n_heavy][ms_nch + 1] first CSR entry of each column chunk (hminsum.cu)

@@ -435,7 +435,11 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   if (m >= (int64_t(1) << 31)) { set_error("too many query rows"); return SD_E_INVALID; }
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t per_warp = int64_t(ix->tile) * int64_t(es) * ((ck == C_KL || ck == C_MAX) ? 2 : 1);
-  const int W = int(std::min<int64_t>(ISECT_MAX_WARPS, (smem_optin_bytes() - 2048) / per_warp));
+  const bool hyb = isect_hybrid_eligible(ix, md, topk);
+  // with the hybrid gather in the sweep's shadow (hybrid.cu) the sweep leaves
+  // room for its 128-thread block on every SM: 12 warps (192 KB, 48 K registers)
+  const int64_t wcap = hyb && knob(SD_TUNE_GATHER_SHADOW) != 0 ? 12 : ISECT_MAX_WARPS;
+  const int W = int(std::min<int64_t>(wcap, (smem_optin_bytes() - 2048) / per_warp));
   if (W < 1) { set_error("index tile does not fit shared memory"); return SD_E_INVALID; }
   const int64_t warps = int64_t(num_sms()) * W;
   // bands of tiles whose postings fit the L2 together, so the index streams
@@ -451,8 +455,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // stream wait for the side streams before these buffers are released)
   Scratch order, tpi, item_off, item_pos, counter, cand_d, cand_i;
   HybridState hs;
-  const bool hyb = isect_hybrid_eligible(ix, md, topk);
-  if (hyb) SD_TRY(hybrid_classify(a, ix, hs, st));
+  if (hyb) SD_TRY(hybrid_classify(a, ix, dtype, hybrid_kind(md->metric), hs, st));
   const int64_t be0 = knob(SD_TUNE_ISECT_BAND);
   // bytes the sweep streams: postings + their (tile, column) ranges (not the
   // hybrid block or the other metric's posting copy, which it never touches)
@@ -549,6 +552,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.b_ptr = b->indptr; args.b_idx = b->indices; args.b_val = static_cast<const T*>(b->values);
     if (tm) tm->begin(PH_PASS1);
     SD_TRY(isect_launch(args, md->metric, W, st));
+    if (hs.nhq > 0 && knob(SD_TUNE_GATHER_SHADOW) != 0) SD_TRY(hybrid_gather(a, b, ix, dtype, hs, st));
     if (tm) tm->end(PH_PASS1);
     if (hs.nhq > 0) {
       if (tm) tm->begin(PH_EXPANSION);  // includes any wait for the side-stream gather

@@ -477,8 +477,9 @@ def test_dense_mode_vs_oracle(shape):
 
 @pytest.mark.parametrize("n_heavy_q", [17, 300])
 def test_hybrid_gemm_routes(n_heavy_q):
-    """The heavy block's GEMM: tcgen05 (<= 256 heavy queries, N = 32 here) and
-    the mma.sync fallback (> 256), both against the oracle (fp32)."""
+    """The heavy block's tcgen05 bf16 GEMM (dense_tc.cu, K split, hi/lo
+    planes) with 128 queries per CTA (17 heavy queries) and 256 per CTA over
+    two query tiles (300), against the oracle (fp32)."""
     idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
     deg = np.diff(np.asarray(idx.indptr))
     heavy = np.flatnonzero(deg >= max(64, -(-idx.n_cols // 32)))
