@@ -41,7 +41,7 @@ static void init_knobs() {
   g_knobs[SD_TUNE_ISECT_L2_DIV] = env("SD_ISECT_L2_DIV", 0);
   g_knobs[SD_TUNE_HEAVY_DEG] = env("SD_HEAVY_DEG", 0);
   g_knobs[SD_TUNE_HYBRID] = env("SD_HYBRID", 1);
-  g_knobs[SD_TUNE_HYBRID_MAX_MB] = env("SD_HYBRID_MAX_MB", 1024);
+  g_knobs[SD_TUNE_HYBRID_MAX_MB] = env("SD_HYBRID_MAX_MB", 8192);
   g_knobs[SD_TUNE_HYBRID_MAX_QUERIES] = env("SD_HYBRID_MAX_QUERIES", 1024);
   g_knobs[SD_TUNE_DENSE] = env("SD_DENSE", 1);
   g_knobs[SD_TUNE_DENSE_MAX_MB] = env("SD_DENSE_MAX_MB", 32768);
@@ -195,7 +195,7 @@ static int fused_run(const sd_csr* a, const sd_csr* b, const sd_index* index, in
     }
     return rc;
   }
-  if (topk == 0 && hybrid_kind(md->metric) >= 0 && hybrid_enabled())
+  if (topk <= 128 && hybrid_kind(md->metric) >= 0 && hybrid_enabled())
     SD_TRY(ensure_hybrid(const_cast<sd_index*>(ix), b, hybrid_kind(md->metric), st));
   const int ph_stats = is_namm(md->metric) ? PH_PASS2 : PH_NORMS;
   tm.begin(ph_stats);

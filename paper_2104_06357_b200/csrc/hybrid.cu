@@ -110,21 +110,7 @@ static int hybrid_base_build(const sd_csr* b, sd_index* ix, cudaStream_t st) {
 // A-operand image
 static int hybrid_dot_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream_t st) {
   const int64_t nh = ix->n_heavy, pad = ix->hpad;
-  const size_t es = dtype == SD_F64 ? 8 : 4;
-  const int64_t dense_bytes = b->n_cols * pad * int64_t(es);
-  if (dense_bytes > knob(SD_TUNE_HYBRID_MAX_MB) << 20) return SD_OK;
-  if (cudaMalloc(&ix->ht, dense_bytes) != cudaSuccess) {
-    set_error("cudaMalloc failed for the hybrid index");
-    return SD_E_CUDA;
-  }
-  SD_CUDA_TRY(cudaMemsetAsync(ix->ht, 0, dense_bytes, st));
-  SD_TRY(SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
-    ht_scatter_kernel<T, false><<<row_scatter_grid(nh), 256, 0, st>>>(
-        b->indptr, b->indices, static_cast<const T*>(b->values), ix->hrows, nh, 128, pad, static_cast<T*>(ix->ht));
-    SD_LAUNCH_CHECK();
-    return SD_OK;
-  }));
-  ix->bytes += dense_bytes;
+  const int64_t cap = knob(SD_TUNE_HYBRID_MAX_MB) << 20;
   if (dtype == SD_F32) {  // the heavy rows as the tcgen05 GEMM's bf16 operand image (dense_tc.cu)
     Scratch flag;
     SD_TRY(flag.alloc(sizeof(unsigned int), st));
@@ -136,16 +122,32 @@ static int hybrid_dot_build(const sd_csr* b, int dtype, sd_index* ix, cudaStream
     const int planes = (inexact & 1u) ? 2 : 1;
     const int64_t nkb = dense_kblocks(b->n_cols);
     const size_t tbytes = dense_image_bytes(nh, nkb, planes, 128);
+    if (int64_t(tbytes) > cap) return SD_OK;
     if (cudaMalloc(&ix->hbf, tbytes) != cudaSuccess) {
       set_error("cudaMalloc failed for the hybrid index (bf16 image)");
       return SD_E_CUDA;
     }
     SD_TRY(dense_image(b, ix->hrows, nh, nkb, planes, 128, ix->hbf, st));
+    SD_CUDA_TRY(cudaStreamSynchronize(st));
     ix->hbf_planes = planes;
     ix->hbf_nkb = nkb;
     ix->bytes += int64_t(tbytes);
+    ix->dot_ready = true;
+    return SD_OK;
   }
+  // fp64: HT, dense column-major, for the CUDA-core DFMA GEMM
+  const int64_t dense_bytes = b->n_cols * pad * 8;
+  if (dense_bytes > cap) return SD_OK;
+  if (cudaMalloc(&ix->ht, dense_bytes) != cudaSuccess) {
+    set_error("cudaMalloc failed for the hybrid index");
+    return SD_E_CUDA;
+  }
+  SD_CUDA_TRY(cudaMemsetAsync(ix->ht, 0, dense_bytes, st));
+  ht_scatter_kernel<double, false><<<row_scatter_grid(nh), 256, 0, st>>>(
+      b->indptr, b->indices, static_cast<const double*>(b->values), ix->hrows, nh, 128, pad, static_cast<double*>(ix->ht));
+  SD_LAUNCH_CHECK();
   SD_CUDA_TRY(cudaStreamSynchronize(st));
+  ix->bytes += dense_bytes;
   ix->dot_ready = true;
   return SD_OK;
 }
@@ -317,121 +319,6 @@ __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__
     V4<T>::store_plain(row + tx * 4, acc[x]);
     V4<T>::store_plain(row + 64 + tx * 4, acc[x] + 4);
   }
-}
-
-// fp32: the same GEMM on the tensor cores with the 3xTF32 split
-// (x = hi + lo, hi = tf32(x), lo = tf32(x - hi); a*b ~ lo_a*hi_b + hi_a*lo_b +
-// hi_a*hi_b, error ~2^-22 |a||b| per product, well inside the fp32 parity
-// tolerance).  mma.sync.m16n8k8 tf32: CTA tile 32 x 128 over BK = 32, four
-// warps of 32 x 32, operands staged K-major in padded shared memory so every
-// fragment load is bank-conflict free.
-constexpr int TG_BM = 32, TG_BN = 128, TG_BK = 32, TG_PA = TG_BM + 8, TG_PB = TG_BN + 8;
-
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
-__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, const uint32_t* b) {
-  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-
-__global__ void __launch_bounds__(128) hgemm_tf32x3_kernel(const float* __restrict__ A, const float* __restrict__ B,
-                                                           int64_t K, int64_t lda, int64_t ldb, int64_t kchunk,
-                                                           int64_t ldp, int64_t rows, float* __restrict__ P) {
-  __shared__ __align__(16) float As[2][TG_BK][TG_PA];
-  __shared__ __align__(16) float Bs[2][TG_BK][TG_PB];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int64_t q0 = int64_t(blockIdx.y) * TG_BM, h0 = int64_t(blockIdx.x) * TG_BN;
-  const int64_t kb = int64_t(blockIdx.z) * kchunk, ke = tmin<int64_t>(K, kb + kchunk);
-  // staging: A tile 32 x 32 (8 floats per thread), B tile 32 x 128 (32 per thread)
-  const int ak = tid >> 2, ac = (tid & 3) * 8;
-  const int bk = tid >> 2, bcol = (tid & 3) * 32;
-  float ra[8], rb[32];
-  auto gload = [&](int64_t k0) {
-    const int64_t k = k0 + ak;
-    if (k < ke) {
-      V4<float>::load(A + k * lda + q0 + ac, ra);
-      V4<float>::load(A + k * lda + q0 + ac + 4, ra + 4);
-#pragma unroll
-      for (int v = 0; v < 8; ++v) V4<float>::load(B + k * ldb + h0 + bcol + 4 * v, rb + 4 * v);
-    } else {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) ra[u] = 0.f;
-#pragma unroll
-      for (int u = 0; u < 32; ++u) rb[u] = 0.f;
-    }
-  };
-  auto sstore = [&](int buf) {
-    V4<float>::store_plain(&As[buf][ak][ac], ra);
-    V4<float>::store_plain(&As[buf][ak][ac + 4], ra + 4);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) V4<float>::store_plain(&Bs[buf][bk][bcol + 4 * v], rb + 4 * v);
-  };
-  float acc[2][4][4];
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[mi][ni][u] = 0.f;
-  gload(kb);
-  sstore(0);
-  __syncthreads();
-  int buf = 0;
-  const int wn = warp * 32;
-  for (int64_t k0 = kb; k0 < ke; k0 += TG_BK) {
-    const bool more = k0 + TG_BK < ke;
-    if (more) gload(k0 + TG_BK);
-#pragma unroll
-    for (int kk = 0; kk < TG_BK; kk += 8) {
-      uint32_t ahi[2][4], alo[2][4];
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const float x[4] = {As[buf][kk + tig][mi * 16 + gid], As[buf][kk + tig][mi * 16 + gid + 8],
-                            As[buf][kk + tig + 4][mi * 16 + gid], As[buf][kk + tig + 4][mi * 16 + gid + 8]};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ahi[mi][u] = to_tf32(x[u]);
-          alo[mi][u] = to_tf32(x[u] - __uint_as_float(ahi[mi][u]));
-        }
-      }
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const float y[2] = {Bs[buf][kk + tig][wn + ni * 8 + gid], Bs[buf][kk + tig + 4][wn + ni * 8 + gid]};
-        uint32_t bhi[2], blo[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          bhi[u] = to_tf32(y[u]);
-          blo[u] = to_tf32(y[u] - __uint_as_float(bhi[u]));
-        }
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          mma_tf32(acc[mi][ni], alo[mi], bhi);
-          mma_tf32(acc[mi][ni], ahi[mi], blo);
-          mma_tf32(acc[mi][ni], ahi[mi], bhi);
-        }
-      }
-    }
-    if (more) {
-      sstore(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
-  }
-  float* out = P + int64_t(blockIdx.z) * rows * ldp;
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int64_t r = q0 + mi * 16 + gid, c = h0 + wn + ni * 8 + 2 * tig;
-      *reinterpret_cast<float2*>(out + r * ldp + c) = make_float2(acc[mi][ni][0], acc[mi][ni][1]);
-      *reinterpret_cast<float2*>(out + (r + 8) * ldp + c) = make_float2(acc[mi][ni][2], acc[mi][ni][3]);
-    }
 }
 
 template <typename T>
@@ -621,15 +508,11 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   }
   // fp32: tcgen05 bf16 GEMM (dense_tc.cu; hi/lo planes where values are
   // not bf16-exact, M = 128 heavy index rows x N = 128 or 256 heavy queries,
-  // K split over ~2 waves of CTAs); mma.sync 3xTF32 (tile 32 x 128 x 32) when
-  // forced; fp64: CUDA-core DFMA (tile 32 x 128 x 16)
-  const int64_t ge = knob(SD_TUNE_HGEMM);  // experiment override: 1 CUDA cores, 2 mma.sync
-  const bool simt = ge == 1;
-  const bool tcb = dtype == SD_F32 && ix->hbf && !simt && ge != 2;
-  const bool tc = dtype == SD_F32 && !simt && !tcb;
+  // K split over ~2 waves of CTAs); fp64: CUDA-core DFMA (tile 32 x 128 x 16)
+  const bool tcb = dtype == SD_F32;
   const int R = hs.nhq <= 128 ? 128 : 256;  // queries per GEMM CTA
-  const int64_t bm = tcb ? R : tc ? TG_BM : HG_BM;
-  const int64_t bn = tcb ? 128 : tc ? TG_BN : HG_BN, bkk = tcb ? 64 : tc ? TG_BK : HG_BK;
+  const int64_t bm = tcb ? R : HG_BM;
+  const int64_t bn = tcb ? 128 : HG_BN, bkk = tcb ? 64 : HG_BK;
   const int64_t tiles_q = (hs.nhq + bm - 1) / bm, tiles_h = ix->hpad / bn;
   const int64_t rows = tcb ? hs.qpad : tiles_q * bm;  // GEMM rows written (<= qpad)
   // K split so that the GEMM fills about two (tensor-core) or six waves of CTAs
@@ -650,15 +533,8 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
     SD_LAUNCH_CHECK();
     const dim3 grid{unsigned(tiles_h), unsigned(tiles_q), unsigned(splits)};
     if constexpr (sizeof(T) == 4) {
-      if (tcb)
-        SD_TRY(dense_gemm_raw(ix->hbf, ix->hbf_planes, ix->n_heavy, hs.hq_img.ptr, q_planes, R, hs.nhq,
-                              ix->hbf_nkb, kchunk / bkk, hs.part.as<float>(), rows, ix->hpad, st));
-      else if (tc)
-        hgemm_tf32x3_kernel<<<grid, 128, 0, st>>>(hs.hqt.as<float>(), static_cast<const float*>(ix->ht), K, hs.qpad,
-                                                  ix->hpad, kchunk, ix->hpad, rows, hs.part.as<float>());
-      else
-        hgemm_kernel<T><<<grid, HG_THREADS, 0, st>>>(hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad,
-                                                     ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());
+      SD_TRY(dense_gemm_raw(ix->hbf, ix->hbf_planes, ix->n_heavy, hs.hq_img.ptr, q_planes, R, hs.nhq,
+                            ix->hbf_nkb, kchunk / bkk, hs.part.as<float>(), rows, ix->hpad, st));
     } else {
       hgemm_kernel<T><<<grid, HG_THREADS, 0, st>>>(hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad,
                                                    ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());

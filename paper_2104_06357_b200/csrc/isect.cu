@@ -365,7 +365,8 @@ int hybrid_kind(int metric) {
 
 bool isect_hybrid_eligible(const sd_index* ix, const sd_metric_desc* md, int topk) {
   const int kind = hybrid_kind(md->metric);
-  if (topk != 0 || kind < 0 || !ix || ix->n_heavy == 0 || !hybrid_enabled()) return false;
+  // kNN too (k <= 128): the heavy queries' dense rows go through a chunked top-k
+  if (topk > 128 || kind < 0 || !ix || ix->n_heavy == 0 || !hybrid_enabled()) return false;
   if (!(kind == HYB_DOT ? ix->dot_ready : ix->ms_ready)) return false;
   return ix->n_tiles >= 4 || hybrid_forced();  // small indexes: the sweep is cheap, keep it exact
 }
@@ -544,6 +545,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.k = T(a->n_cols); args.p = T(md->p);
     args.out = static_cast<T*>(out); args.ldo = ldo; args.flags = flags;
     args.topk = topk;
+    args.heavy_compact = 0;
     args.cand_d = cand_d.as<T>(); args.cand_i = cand_i.as<int64_t>();
     args.a_rank = static_cast<const uint8_t*>(sa.s[2]);
     args.post_rank = ix->post_rank;
@@ -554,14 +556,30 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     SD_TRY(isect_launch(args, md->metric, W, st));
     if (hs.nhq > 0 && knob(SD_TUNE_GATHER_SHADOW) != 0) SD_TRY(hybrid_gather(a, b, ix, dtype, hs, st));
     if (tm) tm->end(PH_PASS1);
+    // kNN: the sweep's per-item lists are merged first (the heavy queries get
+    // empty lists there), then the heavy queries' dense rows are selected
+    if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
     if (hs.nhq > 0) {
       if (tm) tm->begin(PH_EXPANSION);  // includes any wait for the side-stream gather
       SD_TRY(hs.wait(st));
-      SD_TRY(isect_heavy_rows(args, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(), ix->hpad,
-                              hs.dlh.as<T>(), hs.qpad, st));
+      if (topk > 0) {  // dense rows [nhq][n] of the heavy queries, then their top-k
+        const int64_t ldt = (ix->n_rows + 3) / 4 * 4;
+        Scratch rowsbuf;
+        SD_TRY(rowsbuf.alloc(es * size_t(hs.nhq) * size_t(ldt), st));
+        IsectArgs<T> dense_rows = args;
+        dense_rows.out = rowsbuf.as<T>();
+        dense_rows.ldo = ldt;
+        dense_rows.heavy_compact = 1;
+        SD_TRY(isect_heavy_rows(dense_rows, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(),
+                                ix->hpad, hs.dlh.as<T>(), hs.qpad, st));
+        SD_TRY(topk_rows_scatter(rowsbuf.ptr, hs.nhq, ix->n_rows, ldt, dtype, topk, index_base,
+                                 hs.hq.as<int32_t>(), out_d, out_i, st));
+      } else {
+        SD_TRY(isect_heavy_rows(args, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(), ix->hpad,
+                                hs.dlh.as<T>(), hs.qpad, st));
+      }
       if (tm) tm->end(PH_EXPANSION);
     }
-    if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
     return SD_OK;
   });
 }

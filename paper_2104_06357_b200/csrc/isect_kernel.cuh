@@ -54,6 +54,7 @@ struct IsectArgs {
   const int64_t* b_ptr;     // index CSR, for the exact fallback of a fully-hit top-K
   const int32_t* b_idx;
   const T* b_val;
+  int heavy_compact;        // heavy_rows_kernel: output row = heavy id (kNN's dense rows) instead of the query row
 };
 
 // chebyshev hit masks live in the second accumulator array as raw bits
@@ -709,7 +710,7 @@ __global__ void __launch_bounds__(256) heavy_rows_kernel(const IsectArgs<T> a, c
     }
     __syncthreads();
     for (int qq = warp; qq < nhq; qq += int(blockDim.x >> 5)) {
-      const int64_t i = qrow[qq];
+      const int64_t i = a.heavy_compact ? int64_t(qq) : qrow[qq];  // output row (kNN: a compact buffer)
       const T ra0 = qa0[qq];
       const T ra1 = qa1[qq];
       bool fast_zero;

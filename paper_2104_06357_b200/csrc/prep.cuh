@@ -95,6 +95,8 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
               cudaStream_t st);
 int topk_rows(const void* dist, int64_t m, int64_t n, int64_t ldd, int dtype, int k, int64_t base,
               void* od, int64_t* oi, cudaStream_t st);
+int topk_rows_scatter(const void* dist, int64_t m, int64_t n, int64_t ldd, int dtype, int k, int64_t base,
+                      const int32_t* rowmap, void* od, int64_t* oi, cudaStream_t st);
 int topk_merge(const void* cd, const int64_t* ci, int64_t m, int lists, int k, int dtype, void* od,
                int64_t* oi, cudaStream_t st);
 bool metric_two_pass(int metric);

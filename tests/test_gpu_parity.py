@@ -448,6 +448,34 @@ def test_hybrid_minsum_manhattan(dtype, n_heavy_q):
         assert_parity(got, O.pairwise_distances(q, neg, "manhattan"), q, neg, "manhattan", dtype, what="neg index")
 
 
+@pytest.mark.parametrize("k", [7, 40])
+def test_hybrid_knn_heavy_queries(k):
+    """kNN with heavy query rows on the hybrid path: their dense rows (tcgen05
+    GEMM + gather + heavy-row epilogue into a compact buffer) go through the
+    chunked top-k and are scattered into the result; the light queries keep
+    the fused sweep top-k.  Indices equal the oracle's up to ties, and equal
+    the sweep-only path's."""
+    from paper_2104_06357_b200 import _lib
+    idx = _f32(sd.generate(sd.GenSpec(2600, 1600, "zipf", zipf_s=1.15, zipf_max_degree=900, seed=61)))
+    deg = np.diff(np.asarray(idx.indptr))
+    heavy = np.flatnonzero(deg >= max(64, -(-idx.n_cols // 32)))
+    rows = np.unique(np.concatenate([heavy[:30], np.arange(0, idx.n_rows, 53)]))
+    q = _gather_rows(idx, rows)
+    spec = sd.metric_registry("cosine")
+    ref_d, ref_i = O.kneighbors(idx, q, k, "cosine")
+    with _lib.tuned(hybrid=2, dense=0):
+        hidx = _host(idx)
+        res = sd.kneighbors(hidx, _host(q), k, spec, dtype=np.float32)
+        assert "dot" in _lib.device_index(sd.to_device(hidx, np.float32)).hybrid_blocks
+    with _lib.tuned(hybrid=0, dense=0):
+        sweep = sd.kneighbors(_host(idx), _host(q), k, spec, dtype=np.float32)
+    for got in (res, sweep):
+        np.testing.assert_allclose(got.distances, ref_d, rtol=1e-5, atol=1e-5)
+        same = got.indices == ref_i
+        ties = np.abs(got.distances - ref_d) <= 1e-5
+        assert (same | ties).all()
+
+
 @pytest.mark.parametrize("shape", [(300, 517, 700), (130, 129, 64)])
 def test_dense_mode_vs_oracle(shape):
     """Dense-index mode (dense_tc.cu, knob dense=2 forces it on any index):

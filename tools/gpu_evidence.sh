@@ -20,8 +20,13 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 timeout 900 ncu -f --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-check > /dev/null 2>&1
 if [ -z "$SKIP_NCU" ]; then
-  NCU_SPECS=${NCU_SPECS:-"c2:cosine c2:euclidean c2:manhattan c2:cosine:float64 c3:canberra c3:chebyshev c3:jensenshannon c3:kl c4:hellinger c4:jaccard c5:cosine"} \
+  NCU_SPECS=${NCU_SPECS:-"c2:cosine c2:euclidean c2:manhattan c2:cosine:float64 c3:canberra c3:chebyshev c3:jensenshannon c3:kl c5:cosine"} \
     bash tools/gpu_ncu.sh
-  for k in hgemm hgather heavy_rows; do NCU_SPECS=c2:cosine NCU_KERNEL=$k bash tools/gpu_ncu.sh; done
+  for k in dense_tc hgather heavy_rows; do NCU_SPECS=c2:cosine NCU_KERNEL=$k bash tools/gpu_ncu.sh; done
+  for k in hminsum hgather; do NCU_SPECS=c2:manhattan NCU_KERNEL=$k bash tools/gpu_ncu.sh; done
+  NCU_SPECS="c4:hellinger c4:jaccard" NCU_KERNEL=dense_tc bash tools/gpu_ncu.sh
+  bash tools/sanitize.sh
+  timeout 120 python tools/hbm_probe.py > gpurun_out/hbm_probe.json 2>&1
 fi
+for m in cosine manhattan; do timeout 300 python tools/timeline.py --metric $m 2>/dev/null | grep -v "^ *[0-9.]* *[0-9.]* *[0-9.]* *[0-9]* *step$" > gpurun_out/timeline_c2_$m.txt; done
 ls gpurun_out | wc -l

@@ -65,6 +65,16 @@ def main(tag):
             "dram_write_bytes": wr, "duration": vals.get("gpu__time_duration.sum"),
             "source": os.path.relpath(out, ROOT)}
     json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
+    for f in glob.glob(os.path.join(OUT, "sanitize_*.log")):
+        tool = os.path.basename(f)[len("sanitize_"):-len(".log")]
+        lines = open(f).read().splitlines()
+        keep = [l for l in lines if l.startswith("ok ") or "SUMMARY" in l]
+        hdr = f"# compute-sanitizer --tool {tool} (tools/sanitize.sh -> python tools/sanitize_cases.py)\n"
+        open(os.path.join(PROF, f"{tag}_sanitize_{tool}.txt"), "w").write(hdr + "\n".join(keep) + "\n")
+    for name in ("hbm_probe.json", "timeline_c2_cosine.txt", "timeline_c2_manhattan.txt"):
+        f = os.path.join(OUT, name)
+        if os.path.exists(f):
+            open(os.path.join(PROF, f"{tag}_{name}"), "w").write(open(f).read())
 
 
 if __name__ == "__main__":
