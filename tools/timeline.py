@@ -50,11 +50,19 @@ def main():
     flags = _lib.new_flags(dev)
     m, n = dq.n_rows, di.n_rows
     ldo = (n + 3) // 4 * 4
-    out = torch.empty((m, ldo), dtype=tdt, device=dev)
+    knn = wl["kind"] == "knn"
+    k = wl.get("k", 0)
+    out = torch.empty((m, k) if knn else (m, ldo), dtype=tdt, device=dev)
+    oi = torch.empty((m, k), dtype=torch.int64, device=dev) if knn else None
     sh = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
     ca, cb = _lib.csr_struct(dq), _lib.csr_struct(di)
 
     def step():
+        if knn:
+            _lib.check(lib.sd_knn(ctypes.byref(ca), ctypes.byref(cb), ix.handle, _lib.dtype_code(tdt),
+                                  ctypes.byref(md), k, 0, out.data_ptr(), oi.data_ptr(), flags.data_ptr(), sh),
+                       "sd_knn")
+            return
         _lib.check(lib.sd_pairwise(ctypes.byref(ca), ctypes.byref(cb), ix.handle, _lib.dtype_code(tdt),
                                    ctypes.byref(md), ctypes.byref(strat), out.data_ptr(), ldo, flags.data_ptr(),
                                    ctypes.byref(rep), None, sh), "sd_pairwise")
