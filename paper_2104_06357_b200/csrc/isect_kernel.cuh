@@ -566,8 +566,16 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
           }
         }
         if constexpr (KPL > 0) {
+          // one vote per 4 cells: once the list is full almost every cell is
+          // above the k-th distance (!(r > thr) also admits NaN thresholds
+          // and ties, which the exact offers then sort out)
+          bool poss = false;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) top.offer(q + u < nt, r[u], j0 + q + u, a.topk);
+          for (int u = 0; u < 4; ++u) poss |= (q + u < nt) && !(r[u] > top.thr_d);
+          if (__any_sync(FULL, poss)) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) top.offer(q + u < nt, r[u], j0 + q + u, a.topk);
+          }
         } else {
           if (full && vec_out) {
             V4<T>::store(orow + q, r);
