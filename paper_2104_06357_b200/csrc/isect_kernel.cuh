@@ -323,6 +323,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
     isect_zero<T, M>(a, ra0, ra1, fast_zero, zero_val);
     // cosine reads the index-row norms only to resolve an empty query row
     const bool need_sb0 = M != SD_M_COSINE || !(ra0 > T(0));
+    // ... and over scaled postings not even the 1/||b|| (kNN's generic epilogue)
+    const bool need_sb1 = !(M == SD_M_COSINE && a.cos_scaled && ra0 > T(0));
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
     if constexpr (KPL > 0) top.init();
 
@@ -505,7 +507,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
           sts4_zero(acc_s + q * ES, T(0));
           if constexpr (KL) { lds4(cnt_s + q * ES, gcv); sts4_zero(cnt_s + q * ES, T(0)); }
           if constexpr (SB0) { if (need_sb0) V4<T>::load(a.sb0 + j0 + q, gb0); }
-          if constexpr (SB1) V4<T>::load(a.sb1 + j0 + q, gb1);
+          if constexpr (SB1) { if (need_sb1) V4<T>::load(a.sb1 + j0 + q, gb1); }
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               sts(acc_s + (q + u) * ES, T(0));
               if constexpr (KL) { gcv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
               if constexpr (SB0) { if (need_sb0) gb0[u] = a.sb0[j0 + q + u]; }
-              if constexpr (SB1) gb1[u] = a.sb1[j0 + q + u];
+              if constexpr (SB1) { if (need_sb1) gb1[u] = a.sb1[j0 + q + u]; }
             }
           }
         }
@@ -567,11 +569,16 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         }
         if constexpr (KPL > 0) {
           // one vote per 4 cells: once the list is full almost every cell is
-          // above the k-th distance (!(r > thr) also admits NaN thresholds
-          // and ties, which the exact offers then sort out)
+          // above the k-th distance.  Exact admission test: cells arrive in
+          // ascending index within an item, so a cell tying the k-th
+          // distance never precedes it (ties — e.g. the many cosine 1.0s of
+          // cells without intersections — are rejected here); a NaN
+          // threshold means the list is not full yet
+          const T thr = top.thr_d;
+          const bool open = thr != thr;
           bool poss = false;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) poss |= (q + u < nt) && !(r[u] > top.thr_d);
+          for (int u = 0; u < 4; ++u) poss |= (q + u < nt) && (open || r[u] < thr);
           if (__any_sync(FULL, poss)) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) top.offer(q + u < nt, r[u], j0 + q + u, a.topk);
