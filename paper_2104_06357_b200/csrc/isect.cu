@@ -50,6 +50,12 @@ __global__ void index_count_kernel(const int64_t* __restrict__ ptr, const int32_
   }
 }
 
+// kNN: every query's shared k-th-distance bound starts at +inf
+template <typename K>
+__global__ void fill_key_kernel(K* __restrict__ k, int64_t n, K v) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) k[e] = v;
+}
+
 // per-tile sums of row degrees and squared row degrees (collision estimate)
 __global__ void tile_degree_kernel(const int64_t* __restrict__ ptr, int64_t n_rows, int tile, double* sums) {
   for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows; r += int64_t(gridDim.x) * blockDim.x) {
@@ -520,7 +526,15 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     if (tm) tm->end(PH_PASS2);
   }
   if (ps != st) SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.stats_done, 0));
+  Scratch kth;
   if (topk > 0) {
+    SD_TRY(kth.alloc(8 * size_t(m), st));
+    const int blocks = int(std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 4));
+    if (dtype == SD_F64)
+      fill_key_kernel<long long><<<blocks, 256, 0, st>>>(kth.as<long long>(), m, 0x7ff0000000000000LL);
+    else
+      fill_key_kernel<int><<<blocks, 256, 0, st>>>(kth.as<int>(), m, 0x7f800000);
+    SD_LAUNCH_CHECK();
     SD_TRY(cand_d.alloc(es * size_t(max_items) * topk, st));
     SD_TRY(cand_i.alloc(sizeof(int64_t) * size_t(max_items) * topk, st));
   }
@@ -547,6 +561,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.topk = topk;
     args.heavy_compact = 0;
     args.cand_d = cand_d.as<T>(); args.cand_i = cand_i.as<int64_t>();
+    args.kth = kth.as<typename OrdKey<T>::type>();
     args.a_rank = static_cast<const uint8_t*>(sa.s[2]);
     args.post_rank = ix->post_rank;
     args.topa = static_cast<const T*>(sa.s[0]);

@@ -16,6 +16,24 @@ template <typename T> struct Posting;
 template <> struct __align__(8) Posting<float> { uint32_t j; float v; };
 template <> struct __align__(16) Posting<double> { uint32_t j; uint32_t pad; double v; };
 
+// order-preserving integer image of a float (for atomicMin on distances)
+template <typename T> struct OrdKey;
+template <> struct OrdKey<float> {
+  using type = int;
+  __device__ __forceinline__ static int key(float f) { const int b = __float_as_int(f); return b >= 0 ? b : b ^ 0x7fffffff; }
+  __device__ __forceinline__ static float val(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+};
+template <> struct OrdKey<double> {
+  using type = long long;
+  __device__ __forceinline__ static long long key(double f) {
+    const long long b = __double_as_longlong(f);
+    return b >= 0 ? b : b ^ 0x7fffffffffffffffLL;
+  }
+  __device__ __forceinline__ static double val(long long k) {
+    return __longlong_as_double(k >= 0 ? k : k ^ 0x7fffffffffffffffLL);
+  }
+};
+
 template <typename T>
 struct IsectArgs {
   const int64_t* a_ptr;
@@ -55,6 +73,9 @@ struct IsectArgs {
   const int32_t* b_idx;
   const T* b_val;
   int heavy_compact;        // heavy_rows_kernel: output row = heavy id (kNN's dense rows) instead of the query row
+  // kNN: per query, an upper bound of its k-th distance shared by its items
+  // (ordered-integer keys, ord_key), lowered when an item's list fills
+  typename OrdKey<T>::type* kth;
 };
 
 // chebyshev hit masks live in the second accumulator array as raw bits
@@ -327,6 +348,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
     const bool need_sb1 = !(M == SD_M_COSINE && a.cos_scaled && ra0 > T(0));
     WarpTopK<T, (KPL > 0 ? KPL : 1)> top;
     if constexpr (KPL > 0) top.init();
+    // kNN: cells above the query's shared bound cannot reach its top-k (the
+    // bound is some item's k-th distance, >= the final k-th distance)
+    T gbound = Num<T>::inf();
+    if constexpr (KPL > 0) gbound = OrdKey<T>::val(__ldcg(a.kth + i));
 
     // the first 32 columns of the query and their posting ranges in tile t0;
     // later tiles get theirs prefetched during the previous tile's epilogue
@@ -338,6 +363,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
     uint32_t pb0 = valid0 ? a.colptr[t0 * a.n_cols + c0] : 0u;
     uint32_t pe0 = valid0 ? a.colptr[t0 * a.n_cols + c0 + 1] : 0u;
     for (int64_t t = t0; t < t1; ++t) {
+      if constexpr (KPL > 0) gbound = min_(gbound, OrdKey<T>::val(__ldcg(a.kth + i)));  // other items' progress
       const int64_t j0 = t * TJ;
       const int nt = int(tmin<int64_t>(TJ, a.n - j0));
       const uint32_t* cp = a.colptr + t * a.n_cols;
@@ -576,12 +602,15 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
           // threshold means the list is not full yet
           const T thr = top.thr_d;
           const bool open = thr != thr;
-          bool poss = false;
+          bool ok[4], poss = false;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) poss |= (q + u < nt) && (open || r[u] < thr);
+          for (int u = 0; u < 4; ++u) {
+            ok[u] = (q + u < nt) && !(r[u] > gbound);  // (NaN distances only while the bound is open)
+            poss |= ok[u] && (open || r[u] < thr);
+          }
           if (__any_sync(FULL, poss)) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) top.offer(q + u < nt, r[u], j0 + q + u, a.topk);
+            for (int u = 0; u < 4; ++u) top.offer(ok[u], r[u], j0 + q + u, a.topk);
           }
         } else {
           if (full && vec_out) {
@@ -607,8 +636,11 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
       }
       __syncwarp();
     }
-    if constexpr (KPL > 0)
+    if constexpr (KPL > 0) {
       top.store(a.topk, a.cand_d + int64_t(item) * a.topk, a.cand_i + int64_t(item) * a.topk, 0);
+      const T thr = top.thr_d;
+      if (lane == 0 && thr == thr) atomicMin(a.kth + i, OrdKey<T>::key(thr));  // the list is full
+    }
   }
   flags = __reduce_or_sync(FULL, flags);
   if (flags && lane == 0) atomicOr(a.flags, flags);
