@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
 
   // one posting (row jr, value bv) of a column with query value x (and, for
   // chebyshev, query-entry rank xr; jr then carries the posting's rank in bits 16..23)
-  auto apply_posting = [&](uint32_t jr, T bv, T x, uint32_t xr) {
+  auto apply_posting = [&](uint32_t jr, T bv, T x, uint32_t xr, T xl) {
     if constexpr (MX) {
       const uint32_t jl = jr & 0xffffu, rb = jr >> 16;
       const uint32_t ad = acc_s + jl * ES;
@@ -300,7 +300,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
       }
     } else {
       const uint32_t ad = acc_s + jr * ES;
-      sts(ad, add_rn(lds(ad, T(0)), contrib<CK, T>(x, bv, p)));
+      T c;
+      if constexpr (CK == C_JS) c = js_contrib(x, xl, bv);  // log(x) once per column
+      else c = contrib<CK, T>(x, bv, p);
+      sts(ad, add_rn(lds(ad, T(0)), c));
       if constexpr (KL) sts(cnt_s + jr * ES, add_rn(lds(cnt_s + jr * ES, T(0)), T(1)));
     }
   };
@@ -426,7 +429,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
               uint32_t xr = 0;
               if constexpr (MX) xr = __shfl_sync(FULL, cur_ar, (q0 + u) & 31);
-              if (ps[u].j != 0xffffffffu) apply_posting(ps[u].j, ps[u].v, x, xr);
+              const T xl = CK == C_JS ? log_(x) : T(0);
+              if (ps[u].j != 0xffffffffu) apply_posting(ps[u].j, ps[u].v, x, xr, xl);
               __syncwarp();
             }
           } else {
@@ -436,14 +440,15 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                 const T x = __shfl_sync(FULL, cur_av, (q0 + u) & 31);
                 uint32_t xr = 0;
                 if constexpr (MX) xr = __shfl_sync(FULL, cur_ar, (q0 + u) & 31);
-                if (ps[u].j != 0xffffffffu) apply_posting(ps[u].j, ps[u].v, x, xr);
+                const T xl = CK == C_JS ? log_(x) : T(0);
+                if (ps[u].j != 0xffffffffu) apply_posting(ps[u].j, ps[u].v, x, xr, xl);
                 if (long_mask & (1u << ((q0 + u) & 31))) {  // > 32 postings of this column in this tile
                   const uint32_t b0 = __shfl_sync(FULL, cur_pb, (q0 + u) & 31);
                   const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
                   for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
                     Posting<T> q2 = load_posting(post + p2, l2pol);
                     if constexpr (MX) q2.j |= uint32_t(a.post_rank[p2]) << 16;
-                    apply_posting(q2.j, q2.v, x, xr);
+                    apply_posting(q2.j, q2.v, x, xr, xl);
                   }
                 }
                 __syncwarp();

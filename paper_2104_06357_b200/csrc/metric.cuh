@@ -168,6 +168,19 @@ __device__ __forceinline__ T contrib(T a, T b, T p) {
   }
 }
 
+// Jensen-Shannon's intersection term without divisions: with s = x + y,
+// ⊗(x,y) − ⊗(x,0) − ⊗(0,y) = x·log(2x/s) + y·log(2y/s) − (x+y)·log 2
+//                          = x·(log x − log s) + y·(log y − log s)
+// (x, y > 0: stored entries of nonnegative rows); lx = log x is computed once
+// per query column.  Two logs per posting instead of two logs and two
+// divisions; same value up to rounding (the union decomposition is a
+// restatement within tolerance anyway).
+template <typename T>
+__device__ __forceinline__ T js_contrib(T x, T lx, T y) {
+  const T ls = log_(add_rn(x, y));
+  return add_rn(mul_rn(x, sub_rn(lx, ls)), mul_rn(y, sub_rn(log_(y), ls)));
+}
+
 __host__ __device__ constexpr bool is_namm(int metric) {
   return metric >= SD_M_CANBERRA && metric <= SD_M_MINKOWSKI;
 }
