@@ -246,11 +246,13 @@ __global__ void classify_kernel(const int64_t* __restrict__ ptr, int64_t m, int6
 }
 
 // GEMM D = A^T B with A = HQT [K][lda] (heavy queries), B = HT [K][ldb] (heavy
-// index rows), both K-major.  CTA tile 32 x 128, 128 threads with 4 x 8
-// accumulators each (operands read from shared memory as 16-byte vectors), K
+// index rows), both K-major (the fp64 heavy block).  CTA tile 64 x 128, 128
+// threads with 8 x 8 accumulators each (16 operands read from shared memory
+// per 64 FMAs, as 16-byte vectors; 4 x 8 left the kernel shared-memory bound
+// at a sixth of the fp64 peak), K
 // split across blockIdx.z into partial tiles that hreduce_kernel sums in
 // split order (deterministic).
-constexpr int HG_BM = 32, HG_BN = 128, HG_BK = 16, HG_THREADS = 128;
+constexpr int HG_BM = 64, HG_BN = 128, HG_BK = 16, HG_THREADS = 128;
 
 template <typename T>
 __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__ A, const T* __restrict__ B, int64_t K,
@@ -262,30 +264,32 @@ __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t q0 = int64_t(blockIdx.y) * HG_BM, h0 = int64_t(blockIdx.x) * HG_BN;
   const int64_t kb = int64_t(blockIdx.z) * kchunk, ke = tmin<int64_t>(K, kb + kchunk);
-  // global -> register staging: A tile 16 x 32 (4 per thread), B tile 16 x 128 (16 per thread)
-  const int sr = tid >> 3, ac = (tid & 7) * 4, bc = (tid & 7) * 16;
-  T ra[4], rb[16];
+  // global -> register staging: A tile 16 x 64 (8 per thread), B tile 16 x 128 (16 per thread)
+  const int sr = tid >> 3, ac = (tid & 7) * 8, bc = (tid & 7) * 16;
+  T ra[8], rb[16];
   auto gload = [&](int64_t k0) {
     const int64_t k = k0 + sr;
     if (k < ke) {
       V4<T>::load(A + k * lda + q0 + ac, ra);
+      V4<T>::load(A + k * lda + q0 + ac + 4, ra + 4);
 #pragma unroll
       for (int v = 0; v < 4; ++v) V4<T>::load(B + k * ldb + h0 + bc + 4 * v, rb + 4 * v);
     } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) ra[u] = T(0);
+      for (int u = 0; u < 8; ++u) ra[u] = T(0);
 #pragma unroll
       for (int u = 0; u < 16; ++u) rb[u] = T(0);
     }
   };
   auto sstore = [&](int buf) {
     V4<T>::store_plain(&As[buf][sr][ac], ra);
+    V4<T>::store_plain(&As[buf][sr][ac + 4], ra + 4);
 #pragma unroll
     for (int v = 0; v < 4; ++v) V4<T>::store_plain(&Bs[buf][sr][bc + 4 * v], rb + 4 * v);
   };
-  T acc[4][8];
+  T acc[8][8];
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+  for (int x = 0; x < 8; ++x)
 #pragma unroll
     for (int y = 0; y < 8; ++y) acc[x][y] = T(0);
   gload(kb);
@@ -297,12 +301,13 @@ __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__
     if (more) gload(k0 + HG_BK);
 #pragma unroll
     for (int kk = 0; kk < HG_BK; ++kk) {
-      T a[4], b[8];
-      V4<T>::load(&As[buf][kk][ty * 4], a);
+      T a[8], b[8];
+      V4<T>::load(&As[buf][kk][ty * 8], a);
+      V4<T>::load(&As[buf][kk][ty * 8 + 4], a + 4);
       V4<T>::load(&Bs[buf][kk][tx * 4], b);
       V4<T>::load(&Bs[buf][kk][64 + tx * 4], b + 4);
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < 8; ++x)
 #pragma unroll
         for (int y = 0; y < 8; ++y) acc[x][y] = fma_rn(a[x], b[y], acc[x][y]);
     }
@@ -314,8 +319,8 @@ __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__
   }
   T* out = P + int64_t(blockIdx.z) * rows * ldp;
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    T* row = out + (q0 + ty * 4 + x) * ldp + h0;
+  for (int x = 0; x < 8; ++x) {
+    T* row = out + (q0 + ty * 8 + x) * ldp + h0;
     V4<T>::store_plain(row + tx * 4, acc[x]);
     V4<T>::store_plain(row + 64 + tx * 4, acc[x] + 4);
   }
