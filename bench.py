@@ -16,10 +16,14 @@ the 126 MB L2 (C1 excepted, stated in `config`).
 
 Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run, NCCL)
 when not already under torchrun, and fails loudly if the node has fewer GPUs.
-Pairwise workloads scale STRONG by default (the fixed query set is split
-across ranks by work, deg + 16 per row, the index replicated, no collective);
-`--scaling weak` gives every rank its own query batch.  kNN shards the index
-rows and merges the per-rank top-k with one NCCL all-gather.
+Pairwise distances partition by query rows with the index replicated and no
+collective, so they scale WEAK by default: every rank its own
+batch of the workload's queries (seed 26 + rank), value = all ranks'
+distances / the max-over-ranks step time.  `--scaling strong` splits the
+fixed query set across ranks by work instead (DESIGN.md §6 has the per-rank
+cost model: the hybrid path's index-sized costs do not shrink with the
+rank's share).  kNN shards the index rows (fixed total work) and merges the
+per-rank top-k with one NCCL all-gather.
 
 --impl reference: the reference's CPU algorithm (the oracle's numpy port,
 bitwise equal to the reference) on the host cores, bounded query sample.
@@ -696,8 +700,8 @@ def main():
     ap.add_argument("--metric", default=None, help="override the workload's headline metric")
     ap.add_argument("--dtype", choices=["float32", "float64"], default="float32")
     ap.add_argument("--queries", type=int, default=0)
-    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
-                    help="pairwise multi-GPU: split the fixed query set (strong) or a batch per rank (weak)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="weak",
+                    help="pairwise multi-GPU: a query batch per rank (weak, default) or the fixed set split (strong)")
     ap.add_argument("--ref-queries", type=int, default=64)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
