@@ -266,7 +266,11 @@ def pairwise_distances_detail(a, b, spec, strategy=None, workers=None, *, dtype=
     if check_flags:
         _lib.raise_flags(int(flags.item()), name)
     timings = {"norms": phases[0] / 1e3, "pass1": phases[1] / 1e3, "pass2": phases[2] / 1e3,
-               "expansion": phases[3] / 1e3}
+               "expansion": phases[3] / 1e3,
+               # device footprint beside the reference-shaped WorkspaceReport (which restates the
+               # reference's CPU staging plan): the cached index of b and this call's output
+               "device_index_bytes": _lib.device_index(db).bytes if index is not None else 0,
+               "device_output_bytes": int(out_buf.numel() * out_buf.element_size())}
     if host_out is not None:
         dst = host_out if isinstance(host_out, torch.Tensor) else torch.from_numpy(host_out)
         if tuple(dst.shape) != (a.n_rows, b.n_rows):

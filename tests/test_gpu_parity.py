@@ -570,3 +570,14 @@ def test_forced_dense_wider_than_shared_memory(dtype):
         ref = O.pairwise_distances(a, b, name)
         got = sd.pairwise_distances(a, b, sd.metric_registry(name), "dense", dtype=dtype)
         assert_parity(got, ref, a, b, name, dtype, what=f"wide dense {name}")
+
+
+def test_timings_report_device_footprint():
+    """pairwise_distances_detail's timings carry the device footprint beside
+    the reference-shaped WorkspaceReport: the cached index and the output."""
+    a = _host(sd.generate(sd.GenSpec(30, 200, "uniform", degree=10, seed=91)))
+    b = _host(sd.generate(sd.GenSpec(50, 200, "uniform", degree=10, seed=92)))
+    _, report, timings = sd.pairwise_distances_detail(a, b, sd.metric_registry("cosine"), dtype=np.float32)
+    assert timings["device_index_bytes"] > 0
+    assert timings["device_output_bytes"] >= 30 * 50 * 4
+    assert report.peak_accumulator_entries >= 0
