@@ -150,7 +150,7 @@ typedef enum {
   SD_TUNE_HYBRID = 7,          /* SD_HYBRID: 0 off, 1 automatic, 2 forced on small indexes */
   SD_TUNE_HYBRID_MAX_MB = 8,   /* SD_HYBRID_MAX_MB: largest heavy-row image (MiB; fp32 bf16 planes, fp64 HT) */
   SD_TUNE_HYBRID_MAX_QUERIES = 9, /* SD_HYBRID_MAX_QUERIES: heavy query rows per call */
-  SD_TUNE_HGEMM = 10,          /* reserved (round 1's heavy-block GEMM choice; the fp32 block is always tcgen05) */
+  SD_TUNE_HGEMM = 10,          /* SD_HGEMM: fp64 heavy block, 1 = CUDA-core DFMA tile instead of DMMA (fp32: tcgen05) */
   SD_TUNE_DENSE = 11,          /* SD_DENSE: dense-index tensor-core mode, 0 off, 1 automatic, 2 forced */
   SD_TUNE_DENSE_MAX_MB = 12,   /* SD_DENSE_MAX_MB: largest dense index image (MiB) */
   SD_TUNE_GATHER_SHADOW = 13,  /* SD_GATHER_SHADOW (experiment): 1 = hybrid gather co-resident with the sweep

@@ -326,6 +326,89 @@ __global__ void __launch_bounds__(HG_THREADS) hgemm_kernel(const T* __restrict__
   }
 }
 
+// fp64 on the tensor cores: mma.sync m8n8k4 f64 (DMMA).  CTA tile 64
+// (queries) x 128 (heavy index rows), 4 warps of 32 x 64 (4 x 8 MMA tiles,
+// 64 fp64 accumulators per thread), BK = 16 double-buffered through shared
+// memory; fragments: A (8 x 4, row) one element per lane at (lane / 4, lane % 4),
+// B (4 x 8, col) at (lane % 4, lane / 4), C two at (lane / 4, 2 (lane % 4) + {0, 1}).
+constexpr int DM_BM = 64, DM_BN = 128, DM_BK = 8, DM_PA = DM_BM + 4, DM_PB = DM_BN + 4;
+
+__device__ __forceinline__ void dmma(double* c, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) hgemm_dmma_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                         int64_t K, int64_t lda, int64_t ldb, int64_t kchunk,
+                                                         int64_t ldp, int64_t rows, double* __restrict__ P) {
+  __shared__ __align__(16) double As[2][DM_BK][DM_PA];
+  __shared__ __align__(16) double Bs[2][DM_BK][DM_PB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wq = (warp >> 1) * 32, wh = (warp & 1) * 64;  // the warp's 32 x 64 sub-tile
+  const int64_t q0 = int64_t(blockIdx.y) * DM_BM, h0 = int64_t(blockIdx.x) * DM_BN;
+  const int64_t kb = int64_t(blockIdx.z) * kchunk, ke = tmin<int64_t>(K, kb + kchunk);
+  // global -> register staging: A tile 8 x 64 (4 per thread), B tile 8 x 128 (8 per thread)
+  const int sr = tid >> 4, ac = (tid & 15) * 4, bc = (tid & 15) * 8;
+  double ra[4], rb[8];
+  auto gload = [&](int64_t k0) {
+    const int64_t k = k0 + sr;
+    if (k < ke) {
+      V4<double>::load(A + k * lda + q0 + ac, ra);
+      V4<double>::load(B + k * ldb + h0 + bc, rb);
+      V4<double>::load(B + k * ldb + h0 + bc + 4, rb + 4);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ra[u] = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rb[u] = 0.0;
+    }
+  };
+  auto sstore = [&](int buf) {
+    V4<double>::store_plain(&As[buf][sr][ac], ra);
+    V4<double>::store_plain(&Bs[buf][sr][bc], rb);
+    V4<double>::store_plain(&Bs[buf][sr][bc + 4], rb + 4);
+  };
+  double acc[4][8][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  gload(kb);
+  sstore(0);
+  __syncthreads();
+  int buf = 0;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int64_t k0 = kb; k0 < ke; k0 += DM_BK) {
+    const bool more = k0 + DM_BK < ke;
+    if (more) gload(k0 + DM_BK);
+#pragma unroll
+    for (int kk = 0; kk < DM_BK; kk += 4) {
+      double a[4], b[8];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = As[buf][kk + fk][wq + 8 * x + fr];
+#pragma unroll
+      for (int y = 0; y < 8; ++y) b[y] = Bs[buf][kk + fk][wh + 8 * y + fr];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) dmma(acc[x][y], a[x], b[y]);
+    }
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  double* out = P + int64_t(blockIdx.z) * rows * ldp;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int64_t q = q0 + wq + 8 * x + fr;
+#pragma unroll
+    for (int y = 0; y < 8; ++y)
+      *reinterpret_cast<double2*>(out + q * ldp + h0 + wh + 8 * y + 2 * fk) = make_double2(acc[x][y][0], acc[x][y][1]);
+  }
+}
+
 template <typename T>
 __global__ void hreduce_kernel(const T* __restrict__ P, int splits, int64_t count, T* __restrict__ D) {
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
@@ -541,8 +624,13 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
       SD_TRY(dense_gemm_raw(ix->hbf, ix->hbf_planes, ix->n_heavy, hs.hq_img.ptr, q_planes, R, hs.nhq,
                             ix->hbf_nkb, kchunk / bkk, hs.part.as<float>(), rows, ix->hpad, st));
     } else {
-      hgemm_kernel<T><<<grid, HG_THREADS, 0, st>>>(hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad,
-                                                   ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());
+      // fp64: DMMA tensor cores (knob hgemm = 1: the CUDA-core DFMA tile, for A/B)
+      if (knob(SD_TUNE_HGEMM) == 1)
+        hgemm_kernel<T><<<grid, HG_THREADS, 0, st>>>(hs.hqt.as<T>(), static_cast<const T*>(ix->ht), K, hs.qpad,
+                                                     ix->hpad, kchunk, ix->hpad, rows, hs.part.as<T>());
+      else
+        hgemm_dmma_kernel<<<grid, 128, 0, st>>>(hs.hqt.as<double>(), static_cast<const double*>(ix->ht), K, hs.qpad,
+                                                ix->hpad, kchunk, ix->hpad, rows, hs.part.as<double>());
     }
     SD_LAUNCH_CHECK();
     // the gather forks after the GEMM: run side by side they slow each other

@@ -178,7 +178,12 @@ __device__ __forceinline__ T contrib(T a, T b, T p) {
 template <typename T>
 __device__ __forceinline__ T js_contrib(T x, T lx, T y) {
   const T ls = log_(add_rn(x, y));
-  return add_rn(mul_rn(x, sub_rn(lx, ls)), mul_rn(y, sub_rn(log_(y), ls)));
+  const T gen = add_rn(mul_rn(x, sub_rn(lx, ls)), mul_rn(y, sub_rn(log_(y), ls)));
+  // x == y: ⊗(x,x) = 0 exactly, and −x·log 2 − x·log 2 cancels the one-sided
+  // sums (product_a0's x·log 2) bit for bit: identical rows get distance
+  // exactly 0, as in the reference (a select, not a branch: no divergence)
+  const T e = mul_rn(x, log_(T(2)));
+  return x == y ? sub_rn(sub_rn(T(0), e), e) : gen;
 }
 
 __host__ __device__ constexpr bool is_namm(int metric) {

@@ -134,7 +134,10 @@ def kneighbors_detail(index, queries, k, spec, strategy=None, batch_rows=None, w
         d, rep, times = pairwise_distances_detail(batch, dix, spec, strategy, dtype=tdt, return_device=True)
         report = report.merged(rep)
         for key, value in times.items():
-            timings[key] += value
+            if key.startswith("device_"):   # footprints, not times: the largest batch's
+                timings[key] = max(timings.get(key, 0), value)
+            else:
+                timings[key] += value
         t0 = time.perf_counter()
         bd = torch.empty((stop - start, k), dtype=tdt, device=d.device)
         bi = torch.empty((stop - start, k), dtype=torch.int64, device=d.device)
