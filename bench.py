@@ -290,7 +290,9 @@ def run_reference(args):
         "metric": "kNN queries/sec" if k else "pairwise distances/sec", "value": value, "unit": unit,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": (ref["q"] if k else ref["q"] * index.n_rows) / value * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True,
+        "scaling": "strong" if (wl["kind"] == "knn" or args.scaling == "strong") else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, values rounded to fp32)", "impl": "reference",
         "config": {"workload": f"{args.workload}: {metric}, {ref['q']}-query sample vs the full index; {wl['desc']}",
                    "metric": metric, "index_rows": index.n_rows, "n_cols": index.n_cols, "index_nnz": index.nnz},

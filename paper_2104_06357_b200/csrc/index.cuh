@@ -24,7 +24,7 @@ struct sd_index {
   uint32_t* colptr = nullptr;  // [n_tiles * n_cols + 1]
   void* post = nullptr;        // [nnz] Posting<T> (row id within tile, value)
   // chebyshev (built on the first chebyshev call: ensure_cheb)
-  uint8_t* post_rank = nullptr;  // [nnz] rank of the posting's value in its B row (top-CHEB_K, else 255)
+  void* post_cheb = nullptr;   // [nnz] postings with the value's rank in its B row (top-CHEB_K, else 255) in bits 16..23 of j
   void* topb = nullptr;        // [CHEB_K][n_rows] largest |values| per B row
   int64_t bytes = 0;
   // cosine: a copy of `post` with every value divided by its row's L2 norm,

@@ -157,38 +157,43 @@ int index_build(const sd_csr* b, int dtype, int tile, sd_index** out, cudaStream
   return SD_OK;
 }
 
-// rank of every posting's value in its index row (top-CHEB_K by |value|, else
-// 255), from the per-entry ranks: the posting's column follows from its
-// (tile, column) key range, its entry from a binary search in the sorted row
+// chebyshev's copy of the postings with the rank of every posting's value in
+// its index row (top-CHEB_K by |value|, else 255) packed into bits 16..23 of
+// the row id, so the sweep loads one record per posting; the rank comes from
+// the per-entry ranks: the posting's column follows from its (tile, column)
+// key range, its entry from a binary search in the sorted row
 template <typename T>
 __global__ void cheb_rank_kernel(const uint32_t* __restrict__ colptr, const Posting<T>* __restrict__ post,
                                  int64_t n_keys, int64_t n_cols, int tile, const int64_t* __restrict__ bptr,
                                  const int32_t* __restrict__ bidx, const uint8_t* __restrict__ rank,
-                                 uint8_t* __restrict__ post_rank) {
+                                 Posting<T>* __restrict__ post_cheb) {
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n_keys; k += int64_t(gridDim.x) * blockDim.x) {
     const int64_t base = (k / n_cols) * tile;
     const int32_t c = int32_t(k % n_cols);
     for (uint32_t p = colptr[k]; p < colptr[k + 1]; ++p) {
-      const int64_t j = base + post[p].j;
+      Posting<T> q = post[p];
+      const int64_t j = base + q.j;
       int64_t lo = bptr[j], hi = bptr[j + 1];
       while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (bidx[mid] < c) lo = mid + 1; else hi = mid;
       }
-      post_rank[p] = rank[lo];
+      q.j |= uint32_t(rank[lo]) << 16;
+      post_cheb[p] = q;
     }
   }
 }
 
-// Chebyshev's per-row top-CHEB_K |values| and posting ranks, once per index.
+// Chebyshev's per-row top-CHEB_K |values| and ranked postings, once per index.
 int ensure_cheb(sd_index* ix, const sd_csr* b, cudaStream_t st) {
   std::lock_guard<std::mutex> lock(ix->mu);
   if (ix->topb) return SD_OK;
   const size_t es = ix->dtype == SD_F64 ? 8 : 4;
+  const size_t ps = ix->dtype == SD_F64 ? sizeof(Posting<double>) : sizeof(Posting<float>);
   void* topb = nullptr;
-  uint8_t* post_rank = nullptr;
+  void* post_cheb = nullptr;
   if (cudaMalloc(&topb, es * CHEB_K * std::max<int64_t>(1, ix->n_rows)) != cudaSuccess ||
-      cudaMalloc(&post_rank, std::max<int64_t>(1, ix->nnz)) != cudaSuccess) {
+      cudaMalloc(&post_cheb, ps * std::max<int64_t>(1, ix->nnz)) != cudaSuccess) {
     if (topb) cudaFree(topb);
     set_error("cudaMalloc failed for the chebyshev masks");
     return SD_E_CUDA;
@@ -202,15 +207,15 @@ int ensure_cheb(sd_index* ix, const sd_csr* b, cudaStream_t st) {
     rc = SD_DISPATCH_DTYPE(ix->dtype, T, [&]() -> int {
       cheb_rank_kernel<T><<<std::max(1, blocks), 256, 0, st>>>(ix->colptr, static_cast<const Posting<T>*>(ix->post),
                                                                n_keys, ix->n_cols, ix->tile, b->indptr, b->indices,
-                                                               rank.as<uint8_t>(), post_rank);
+                                                               rank.as<uint8_t>(), static_cast<Posting<T>*>(post_cheb));
       SD_LAUNCH_CHECK();
       return SD_OK;
     });
   }
-  if (rc != SD_OK) { cudaFree(topb); cudaFree(post_rank); return rc; }
+  if (rc != SD_OK) { cudaFree(topb); cudaFree(post_cheb); return rc; }
   ix->topb = topb;
-  ix->post_rank = post_rank;
-  ix->bytes += int64_t(es * CHEB_K * ix->n_rows + ix->nnz);
+  ix->post_cheb = post_cheb;
+  ix->bytes += int64_t(es * CHEB_K * ix->n_rows + ps * ix->nnz);
   return SD_OK;
 }
 
@@ -563,7 +568,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.cand_d = cand_d.as<T>(); args.cand_i = cand_i.as<int64_t>();
     args.kth = kth.as<typename OrdKey<T>::type>();
     args.a_rank = static_cast<const uint8_t*>(sa.s[2]);
-    args.post_rank = ix->post_rank;
+    if (md->metric == SD_M_CHEBYSHEV) args.post = static_cast<const Posting<T>*>(ix->post_cheb);
     args.topa = static_cast<const T*>(sa.s[0]);
     args.topb = static_cast<const T*>(ix->topb);
     args.b_ptr = b->indptr; args.b_idx = b->indices; args.b_val = static_cast<const T*>(b->values);
@@ -605,7 +610,7 @@ int sd_index_free(sd_index* ix) {
   if (!ix) return SD_OK;
   if (ix->colptr) cudaFree(ix->colptr);
   if (ix->post) cudaFree(ix->post);
-  if (ix->post_rank) cudaFree(ix->post_rank);
+  if (ix->post_cheb) cudaFree(ix->post_cheb);
   if (ix->topb) cudaFree(ix->topb);
   if (ix->post_cos) cudaFree(ix->post_cos);
   if (ix->dimg) cudaFree(ix->dimg);

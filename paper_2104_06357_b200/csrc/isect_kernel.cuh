@@ -66,7 +66,6 @@ struct IsectArgs {
   int64_t* cand_i;
   // fused chebyshev (C_MAX)
   const uint8_t* a_rank;    // rank of each A entry in its row (top-CHEB_K by |a|, else 255)
-  const uint8_t* post_rank; // rank of each posting's value in its B row
   const T* topa;            // [CHEB_K][m] largest |a| per query row
   const T* topb;            // [CHEB_K][n] largest |b| per index row
   const int64_t* b_ptr;     // index CSR, for the exact fallback of a fully-hit top-K
@@ -402,7 +401,6 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               ps[u].j = 0xffffffffu;
               if (pp < b1) {
                 ps[u] = load_posting(post + pp, l2pol);
-                if constexpr (MX) ps[u].j |= uint32_t(a.post_rank[pp]) << 16;
               }
             }
           } else {
@@ -414,7 +412,6 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               ps[u].j = 0xffffffffu;
               if (q0 + u < ncol && pp < b1) {
                 ps[u] = load_posting(post + pp, l2pol);
-                if constexpr (MX) ps[u].j |= uint32_t(a.post_rank[pp]) << 16;
               }
             }
           }
@@ -447,7 +444,6 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                   const uint32_t b1 = __shfl_sync(FULL, cur_pe, (q0 + u) & 31);
                   for (uint32_t p2 = b0 + 32 + lane; p2 < b1; p2 += 32) {
                     Posting<T> q2 = load_posting(post + p2, l2pol);
-                    if constexpr (MX) q2.j |= uint32_t(a.post_rank[p2]) << 16;
                     apply_posting(q2.j, q2.v, x, xr, xl);
                   }
                 }
