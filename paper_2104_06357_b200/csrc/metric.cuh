@@ -156,6 +156,16 @@ __device__ __forceinline__ T contrib(T a, T b, T p) {
     return product<SD_SR_KL_TERM, T>(a, b, p);
   } else if constexpr (CK == C_MAX) {
     return abs_(sub_rn(a, b));
+  } else if constexpr (CK == C_CANBERRA && sizeof(T) == 4) {
+    // fp32 fused path: |a-b| / (|a|+|b|) with the fast reciprocal-multiply
+    // division (<= 2 ulp of a ratio in [0, 1], inside the fp32 tolerance; the
+    // IEEE division's special-case branch dominated the posting loop), huge
+    // pairs pre-scaled so the approximate divide stays in range; equal values
+    // still give exactly -2 (0 / d = 0)
+    const T num = abs_(sub_rn(a, b)), den = add_rn(abs_(a), abs_(b));
+    const T sc = den > T(1e30) ? T(0x1p-64) : T(1);
+    const T r = den > T(0) ? __fdividef(num * sc, den * sc) : T(0);
+    return sub_rn(sub_rn(r, product_a0<SD_SR_CANBERRA, T>(a, p)), product_0b<SD_SR_CANBERRA, T>(b, p));
   } else {
     constexpr int SR = CK == C_ABS ? SD_SR_ABS_DIFF
                      : CK == C_ABSPOW ? SD_SR_ABS_DIFF_POW
