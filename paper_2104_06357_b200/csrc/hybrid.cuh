@@ -11,6 +11,7 @@ struct HybridState {
   cudaEvent_t join = nullptr;
   cudaStream_t main = nullptr;  // the caller's stream (scratch below is freed on it)
   cudaEvent_t cls = nullptr;         // classification done (side-stream plan / statistics start)
+  cudaEvent_t dense_done = nullptr;  // the dense block's sums complete on the caller's stream
   cudaEvent_t stats_done = nullptr;  // deferred query statistics + work plan (isect_run) finished
   // the caller's stream waits for the side stream (before heavy_rows and
   // before any of this state's scratch is released on it)
@@ -23,6 +24,7 @@ struct HybridState {
     if (stats_done && main) cudaStreamWaitEvent(main, stats_done, 0);
     if (fork) cudaEventDestroy(fork);
     if (cls) cudaEventDestroy(cls);
+    if (dense_done) cudaEventDestroy(dense_done);
     if (stats_done) cudaEventDestroy(stats_done);
     if (join) cudaEventDestroy(join);
   }

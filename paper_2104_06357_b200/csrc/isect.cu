@@ -529,6 +529,10 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     if (tm) tm->begin(PH_PASS2);
     SD_TRY(hybrid_prepare(a, b, ix, dtype, hybrid_kind(md->metric), hs, st));
     if (tm) tm->end(PH_PASS2);
+    if (hs.nhq > 0 && hs.join) {  // the dense block's sums (dqh) are complete at this point of st
+      SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.dense_done, cudaEventDisableTiming));
+      SD_CUDA_TRY(cudaEventRecord(hs.dense_done, st));
+    }
   }
   if (ps != st) SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.stats_done, 0));
   Scratch kth;
@@ -574,12 +578,23 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
     args.b_ptr = b->indptr; args.b_idx = b->indices; args.b_val = static_cast<const T*>(b->values);
     if (tm) tm->begin(PH_PASS1);
     SD_TRY(isect_launch(args, md->metric, W, st));
+    // pairwise: the heavy rows' epilogue writes rows the sweep does not touch —
+    // on side stream 0 after the gather and the dense block, it fills the SMs
+    // the sweep's CTAs release at its tail instead of waiting for all of them
+    if (topk == 0 && hs.nhq > 0 && hs.dense_done) {
+      cudaStream_t side = side_stream(0);
+      SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.dense_done, 0));
+      SD_TRY(isect_heavy_rows(args, md->metric, hs.hq.as<int32_t>(), hs.nhq, ix->hid, hs.dqh.as<T>(), ix->hpad,
+                              hs.dlh.as<T>(), hs.qpad, side));
+      SD_CUDA_TRY(cudaEventRecord(hs.join, side));  // (re-recorded: the caller's stream joins below)
+      SD_CUDA_TRY(cudaStreamWaitEvent(st, hs.join, 0));
+    }
     if (hs.nhq > 0 && knob(SD_TUNE_GATHER_SHADOW) != 0) SD_TRY(hybrid_gather(a, b, ix, dtype, hs, st));
     if (tm) tm->end(PH_PASS1);
     // kNN: the sweep's per-item lists are merged first (the heavy queries get
     // empty lists there), then the heavy queries' dense rows are selected
     if (topk > 0) SD_TRY(isect_merge(args, index_base, static_cast<T*>(out_d), out_i, st));
-    if (hs.nhq > 0) {
+    if (hs.nhq > 0 && !(topk == 0 && hs.dense_done)) {
       if (tm) tm->begin(PH_EXPANSION);  // includes any wait for the side-stream gather
       SD_TRY(hs.wait(st));
       if (topk > 0) {  // dense rows [nhq][n] of the heavy queries, then their top-k
