@@ -156,7 +156,8 @@ typedef enum {
   SD_TUNE_GATHER_SHADOW = 13,  /* SD_GATHER_SHADOW (experiment): 1 = hybrid gather co-resident with the sweep
                                   (one 128-thread block per SM, sweep capped at 12 warps); default 0 = gather on
                                   every SM first (C2 cosine 1.98 ms vs 3.66 ms co-resident) */
-  SD_TUNE_COUNT = 14
+  SD_TUNE_GATHER_BLOCKS = 14,  /* SD_GATHER_BLOCKS: hybrid gather 256-thread blocks per SM, 0 = as many as fit */
+  SD_TUNE_COUNT = 15
 } sd_tune_knob;
 
 /* ---------------------------------------------------------------- misc */

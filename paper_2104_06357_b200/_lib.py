@@ -110,7 +110,7 @@ SIGNATURES = [
 TUNE_KNOBS = {
     "tile": 0, "isect_plan": 1, "cos_raw": 2, "isect_debug": 3, "isect_band": 4, "isect_l2_div": 5,
     "heavy_deg": 6, "hybrid": 7, "hybrid_max_mb": 8, "hybrid_max_queries": 9, "hgemm": 10,
-    "dense": 11, "dense_max_mb": 12, "gather_shadow": 13,
+    "dense": 11, "dense_max_mb": 12, "gather_shadow": 13, "gather_blocks": 14,
 }
 
 _LIB = None

@@ -46,6 +46,7 @@ static void init_knobs() {
   g_knobs[SD_TUNE_DENSE] = env("SD_DENSE", 1);
   g_knobs[SD_TUNE_DENSE_MAX_MB] = env("SD_DENSE_MAX_MB", 32768);
   g_knobs[SD_TUNE_GATHER_SHADOW] = env("SD_GATHER_SHADOW", 0);
+  g_knobs[SD_TUNE_GATHER_BLOCKS] = env("SD_GATHER_BLOCKS", 0);
   const char* g = getenv("SD_HGEMM");
   g_knobs[SD_TUNE_HGEMM] = !g ? 0 : std::string(g) == "simt" ? 1 : std::string(g) == "mma" ? 2 : atoll(g);
 }

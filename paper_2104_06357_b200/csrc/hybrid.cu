@@ -431,7 +431,7 @@ constexpr int HGU = SD_HGATHER_UNROLL;
 // D + blk * bstride + c * ld.  Rows are taken from a shared counter in
 // descending-degree order (lrows, index build) so the long rows start first
 // and no warp is left with a tail of them.
-template <typename T, bool MINSUM>
+template <typename T, bool MINSUM, int QPL>
 __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                       const T* __restrict__ val, const int32_t* __restrict__ lrows,
                                                       int64_t n_light, const T* __restrict__ D, int64_t ld,
@@ -446,32 +446,38 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
     if (it >= total) break;
     const int64_t j = lrows[it / nblk], blk = int64_t(it % nblk);
     const int64_t beg = ptr[j], end = ptr[j + 1];
-    const T* dcol = D + blk * bstride + 4 * lane;
-    T acc[4] = {T(0), T(0), T(0), T(0)};
+    const T* dcol = D + blk * bstride + QPL * lane;
+    T acc[QPL];
+#pragma unroll
+    for (int k = 0; k < QPL; ++k) acc[k] = T(0);
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
       const bool ok = e0 + lane < end;
       const int32_t cl = ok ? idx[e0 + lane] : 0;
       const T vl = ok ? val[e0 + lane] : T(0);
       const int nn = int(tmin<int64_t>(32, end - e0));
       for (int u0 = 0; u0 < nn; u0 += HGU) {
-        T d[HGU][4];
+        T d[HGU][QPL];
         T x[HGU];
 #pragma unroll
         for (int u = 0; u < HGU; ++u) {
           const int src = (u0 + u) & 31;
           const int32_t c = __shfl_sync(0xffffffffu, cl, src);
           x[u] = __shfl_sync(0xffffffffu, vl, src);
-          if (u0 + u < nn) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
+          if (u0 + u < nn) {
+            if constexpr (QPL == 4) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
+            else d[u][0] = dcol[int64_t(c) * ld];
+          }
         }
 #pragma unroll
         for (int u = 0; u < HGU; ++u)
           if (u0 + u < nn)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < QPL; ++k)
               acc[k] = MINSUM ? add_rn(acc[k], min_(x[u], d[u][k])) : fma_rn(x[u], d[u][k], acc[k]);
       }
     }
-    V4<T>::store_plain(out + j * ldo + blk * 128 + 4 * lane, acc);
+    if constexpr (QPL == 4) V4<T>::store_plain(out + j * ldo + blk * 128 + 4 * lane, acc);
+    else out[j * ldo + blk * 32 + lane] = acc[0];
   }
 }
 
@@ -502,39 +508,38 @@ int hybrid_classify(const sd_csr* a, const sd_index* ix, int dtype, int kind, Hy
 int hybrid_gather(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, HybridState& hs, cudaStream_t st) {
   if (hs.nhq == 0) return SD_OK;
   const bool ms = hs.gather_kind == HYB_MINSUM;
-  const int64_t K = a->n_cols, nblk = hs.qpad / 128;
-  const int64_t hq_bstride = ms ? K * 128 : 128, hq_ld = ms ? 128 : hs.qpad;
+  const int qpl = hs.qpad % 128 == 0 ? 4 : 1;  // queries per lane: 128-query blocks, or one block of 32
+  const int64_t K = a->n_cols, nblk = hs.qpad / (32 * qpl);
+  const int64_t hq_bstride = ms ? K * 128 : 32 * qpl, hq_ld = ms ? 128 : hs.qpad;
   cudaStream_t side = hs.fork ? side_stream(0) : st;
   if (side != st) SD_CUDA_TRY(cudaStreamWaitEvent(side, hs.fork, 0));
   // keep the SMs' shared-memory carveout at its maximum while the gather
   // runs, so CTAs needing ~200 KB of shared memory can co-reside with it
   static const bool carve = [] {
-    cudaFuncSetAttribute(hgather_kernel<float, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(hgather_kernel<float, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(hgather_kernel<double, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(hgather_kernel<double, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<float, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<float, false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<float, true, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<double, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hgather_kernel<double, true, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return true;
   }();
   (void)carve;
   const bool shadow = knob(SD_TUNE_GATHER_SHADOW) != 0;
   const int gthreads = shadow ? 128 : 256;
   SD_TRY(SD_DISPATCH_DTYPE(dtype, T, [&]() -> int {
-    int per_sm = 0;
-    if (ms) {
-      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, true>, 256, 0));
+    auto go = [&](auto kernel) -> int {
+      int per_sm = 0;
+      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
       if (shadow) per_sm = 1;
-      hgather_kernel<T, true><<<std::max(1, per_sm) * num_sms(), gthreads, 0, side>>>(
+      else if (knob(SD_TUNE_GATHER_BLOCKS) > 0) per_sm = std::min<int>(per_sm, int(knob(SD_TUNE_GATHER_BLOCKS)));
+      kernel<<<std::max(1, per_sm) * num_sms(), gthreads, 0, side>>>(
           b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
           hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
-    } else {
-      SD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hgather_kernel<T, false>, 256, 0));
-      if (shadow) per_sm = 1;
-      hgather_kernel<T, false><<<std::max(1, per_sm) * num_sms(), gthreads, 0, side>>>(
-          b->indptr, b->indices, static_cast<const T*>(b->values), ix->lrows, ix->n_light, hs.hqt.as<T>(), hq_ld,
-          hq_bstride, nblk, hs.qpad, hs.gcount.as<unsigned long long>(), hs.dlh.as<T>());
-    }
-    SD_LAUNCH_CHECK();
-    return SD_OK;
+      SD_LAUNCH_CHECK();
+      return SD_OK;
+    };
+    if (ms) return go(hgather_kernel<T, true, 4>);
+    return qpl == 4 ? go(hgather_kernel<T, false, 4>) : go(hgather_kernel<T, false, 1>);
   }));
   if (side != st) {
     SD_CUDA_TRY(cudaEventCreateWithFlags(&hs.join, cudaEventDisableTiming));
@@ -555,8 +560,11 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   if (hs.nhq == 0) return SD_OK;
   const size_t es = dtype == SD_F64 ? 8 : 4;
   const int64_t K = a->n_cols;
-  hs.qpad = (hs.nhq + 127) / 128 * 128;
-  const int64_t nblk = hs.qpad / 128;
+  // a few heavy queries (e.g. one rank's share of a strong-scaled run, fp32
+  // dot family): one 32-query block, so the gather reads 128 B of HQT per
+  // index entry instead of 512 (the min-sum block stages 128-query chunks and
+  // the fp64 GEMM tiles 64 queries)
+  hs.qpad = (kind != HYB_MINSUM && dtype == SD_F32 && hs.nhq <= 32) ? 32 : (hs.nhq + 127) / 128 * 128;
   SD_TRY(hs.hqt.alloc(es * size_t(K) * size_t(hs.qpad), st));
   SD_CUDA_TRY(cudaMemsetAsync(hs.hqt.ptr, 0, es * size_t(K) * size_t(hs.qpad), st));
   SD_TRY(hs.dqh.alloc(es * size_t(hs.qpad) * size_t(ix->hpad), st));
@@ -564,7 +572,7 @@ int hybrid_prepare(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dty
   // min-sum: HQT in 128-query blocks ([blk][K][128], one contiguous stage per
   // column chunk for the bulk copies of hminsum_kernel) holding max(a, 0)
   const bool ms = kind == HYB_MINSUM;
-  const int64_t hq_bstride = ms ? K * 128 : 128, hq_ld = ms ? 128 : hs.qpad;
+  const int64_t hq_bstride = ms ? K * 128 : (hs.qpad % 128 == 0 ? 128 : 32), hq_ld = ms ? 128 : hs.qpad;
   // the dense gather runs on a side stream (heavy_rows joins it), after the
   // dense block
   // the gather forks now (it only needs HQT).  Shadow mode (knob, off by

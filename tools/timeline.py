@@ -25,6 +25,9 @@ def main():
     ap.add_argument("--metric", default="cosine")
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--queries", type=int, default=0, help="query rows (default: the workload's)")
+    ap.add_argument("--api", type=float, default=0.0,
+                    help="also list CUDA runtime calls on the host longer than this many us")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -35,7 +38,7 @@ def main():
 
     wl = bench.WORKLOADS[args.workload]
     index = bench.make_index(wl)
-    queries = bench.make_queries(wl, index, wl["n_queries"])
+    queries = bench.make_queries(wl, index, args.queries or wl["n_queries"])
     idx_m, q_m = bench.operands_for(args.metric, index, queries)
     tdt = torch.float32 if args.dtype == "float32" else torch.float64
     dev = torch.device("cuda", 0)
@@ -75,8 +78,11 @@ def main():
             with torch.profiler.record_function("step"):
                 step()
         torch.cuda.synchronize()
-    evs = []
+    evs, api = [], []
     for e in prof.events():
+        if (args.api > 0 and e.device_type == torch.autograd.DeviceType.CPU and e.name.startswith("cuda")
+                and e.time_range.end - e.time_range.start >= args.api):
+            api.append((e.time_range.start, e.time_range.end, -1, "host " + e.name))
         if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.end > e.time_range.start:
             evs.append((e.time_range.start, e.time_range.end, getattr(e, "device_resource_id", 0) or 0, e.name))
     evs.sort()
@@ -89,10 +95,11 @@ def main():
     t0 = last[0][0]
     print(f"# {args.workload} {args.metric} {args.dtype}: last of {args.steps} profiled steps, "
           f"{len(last)} device activities, span {(last[-1][1] - t0) / 1e3:.3f} ms")
+    last = sorted(last + [a for a in api if last[0][0] - 500 <= a[0] <= last[-1][1]])
     print(f"{'start_us':>9} {'end_us':>9} {'dur_us':>8} stream  name")
     for s, e, r, name in last:
         print(f"{(s - t0):9.1f} {(e - t0):9.1f} {(e - s):8.1f} {r:6d}  {name[:90]}")
-    ends = np.array([e for _, e, _, _ in last])
+    ends = np.array([e for _, e, r, _ in last if r >= 0])
     print(f"# step span {(ends.max() - t0) / 1e3:.3f} ms")
 
 
