@@ -478,14 +478,17 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   // about a fifth of the L2 (C2 cosine: bands of 100 MB 2.37 ms, 50 MB 2.28,
   // 25 MB 2.21, 12 MB 2.43) — the rest holds the streaming output.
   // Otherwise whole-L2 bands: with heavy rows in the sweep (C2 manhattan 4.9
-  // vs 5.9 ms) and for kNN, where every band adds a top-k list per query to
-  // merge (C5: 49 vs 56 ms), smaller bands cost more than they save.
+  // vs 5.9 ms) smaller bands cost more than they save.
   const int64_t ld = knob(SD_TUNE_ISECT_L2_DIV);
   // Dense-ish indexes (long posting lists per (tile, column), C4: ~280) also
   // prefer the small bands (C4 46.4 -> 39.6 ms).
   const bool long_lists = ix->nnz > 64 * ix->n_tiles * ix->n_cols;
   const int64_t div = ld > 0 ? ld : (topk == 0 && (hyb || long_lists) ? 5 : 1);
-  const int64_t band_bytes = std::max<int64_t>(1, l2_bytes() / std::max<int64_t>(1, div));
+  // kNN: bands of ~2.5 L2 — every item of a band starts an empty top-k list
+  // and leaves one to merge, so fewer, longer items win over L2 residency
+  // (C5 with the shared bound: 1 L2 23.1 ms, 2.5 L2 21.6, whole index 22.3)
+  const int64_t band_bytes = std::max<int64_t>(
+      1, topk > 0 && ld <= 0 ? l2_bytes() * 5 / 2 : l2_bytes() / std::max<int64_t>(1, div));
   const int64_t n_bands0 = (post_bytes + band_bytes - 1) / band_bytes;
   const int64_t auto_band = (ix->n_tiles + n_bands0 - 1) / n_bands0;
   const int64_t band0 = std::max<int64_t>(1, std::min<int64_t>(ix->n_tiles, be0 > 0 ? be0 : auto_band));

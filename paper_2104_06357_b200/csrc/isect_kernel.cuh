@@ -458,17 +458,18 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         pe0 = valid0 ? cp[a.n_cols + c0 + 1] : 0u;
       }
       if (a.debug & 2) continue;
-      if constexpr (KPL == 0 && !MX) {
-        // full tile, 16-byte aligned output rows: a straight-line epilogue with
-        // pointers advanced per group, no bounds tests, and the per-query
-        // cosine branch hoisted out of the cell loop
-        if (vec_out && nt == TJ && TJ % (EPF * 128) == 0) {
+      if constexpr (!MX) {
+        // full tile (and, pairwise, 16-byte aligned output rows): a
+        // straight-line epilogue with pointers advanced per group, no bounds
+        // tests, and the per-query cosine branch hoisted out of the cell loop;
+        // kNN votes each group against its bounds instead of storing it
+        if ((KPL > 0 || vec_out) && nt == TJ && TJ % (EPF * 128) == 0) {
           // nz: 0 generic cell, 1 cosine of a non-empty query, 2 the same over
           // scaled postings (no per-cell index statistic at all)
           auto run = [&](auto nz) {
             constexpr int NZM = decltype(nz)::value;
             constexpr bool NZ = NZM > 0;
-            T* op = a.out + i * a.ldo + j0 + 4 * lane;
+            T* op = KPL == 0 ? a.out + i * a.ldo + j0 + 4 * lane : nullptr;
             const T* p0 = SB0 ? a.sb0 + j0 + 4 * lane : nullptr;
             const T* p1 = SB1 ? a.sb1 + j0 + 4 * lane : nullptr;
             uint32_t sa = acc_s + 4u * uint32_t(lane) * ES;
@@ -498,7 +499,22 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                   flags |= f;
                 }
               }
-              V4<T>::store(op + off, r);
+              if constexpr (KPL > 0) {  // the generic epilogue's vote (below), same bounds
+                const T thr = top.thr_d;
+                const bool open = thr != thr;
+                bool ok[4], poss = false;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  ok[u] = !(r[u] > gbound);
+                  poss |= ok[u] && (open || r[u] < thr);
+                }
+                if (__any_sync(FULL, poss)) {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) top.offer(ok[u], r[u], j0 + off + 4 * lane + u, a.topk);
+                }
+              } else {
+                V4<T>::store(op + off, r);
+              }
             };
 #pragma unroll
             for (int q = 0; q < EPF; ++q) load(uint32_t(q) * 128u, gv[q], gc[q], g0[q], g1[q]);
