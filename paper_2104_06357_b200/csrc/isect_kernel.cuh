@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
   // posting schedule, chosen per instantiation (both in one kernel cost
   // registers and instruction cache): flattened waves where the per-posting
   // work is heavy or the epilogue light enough for the sweep to dominate
-  // (JS 11.6 -> 7.7 ms, canberra 8.5 -> 8.0 on C3; kNN C5 23.0 -> 16.4);
-  // column at a time for the rest (C2 cosine 1.44 vs 2.02 ms flattened,
-  // manhattan 1.80 vs 2.33, chebyshev 15.4 vs 17.9, KL even)
-  constexpr bool FLAT = KPL > 0 || CK == C_JS || CK == C_CANBERRA;
+  // (JS 11.6 -> 7.7 ms, canberra 8.5 -> 7.9, KL 15.4 -> 13.1 on C3; kNN C5
+  // 23.0 -> 15.1); column at a time for the rest (C2 cosine 1.42 vs 2.02 ms
+  // flattened, manhattan 1.80 vs 2.33, chebyshev 15.5 vs 16.0)
+  constexpr bool FLAT = KPL > 0 || CK == C_JS || CK == C_CANBERRA || CK == C_KL;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int TJ = a.tile;
@@ -436,18 +436,39 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               ps[u].j = 0xffffffffu;
               if (f < total) ps[u] = load_posting(post + pbk + (f - ok0), l2pol);
             }
+            // conflicts: lanes of a wave holding the same row apply in column
+            // order.  KL (7 warps per SM, two accumulator arrays) ranks all UW
+            // waves first so the match instructions overlap (C3 14.8 -> 13.1
+            // ms); the lighter metrics lose to the extra registers (JS 7.6 ->
+            // 8.3) and rank wave by wave
+            constexpr bool HOIST = CK == C_KL;
+            int rk[UW];
+            bool conflict = false;
+            if constexpr (HOIST) {
+              unsigned any_rank = 0;
+#pragma unroll
+              for (int u = 0; u < UW; ++u) {
+                const bool act = ps[u].j != 0xffffffffu;
+                const uint32_t key = act ? (MX ? (ps[u].j & 0xffffu) : ps[u].j) : (0xffff0000u | uint32_t(lane));
+                rk[u] = __popc(__match_any_sync(FULL, key) & ((1u << lane) - 1u));
+                any_rank |= unsigned(rk[u]);
+              }
+              conflict = __any_sync(FULL, any_rank != 0u);
+            }
 #pragma unroll
             for (int u = 0; u < UW; ++u) {
               if (w0 + 32u * uint32_t(u) < total) {  // warp-uniform
                 const bool act = ps[u].j != 0xffffffffu;
                 const T xl = CK == C_JS ? log_(xs[u]) : T(0);
-                const uint32_t key = act ? (MX ? (ps[u].j & 0xffffu) : ps[u].j) : (0xffff0000u | uint32_t(lane));
-                const unsigned mm = __match_any_sync(FULL, key);
-                const int rank = __popc(mm & ((1u << lane) - 1u));
-                if (__any_sync(FULL, rank > 0)) {  // the same row twice in this wave: in column order
-                  const int maxr = __reduce_max_sync(FULL, unsigned(rank));
+                if constexpr (!HOIST) {
+                  const uint32_t key = act ? (MX ? (ps[u].j & 0xffffu) : ps[u].j) : (0xffff0000u | uint32_t(lane));
+                  rk[u] = __popc(__match_any_sync(FULL, key) & ((1u << lane) - 1u));
+                  conflict = __any_sync(FULL, rk[u] > 0);
+                }
+                if (conflict) {
+                  const int maxr = int(__reduce_max_sync(FULL, unsigned(rk[u])));
                   for (int r = 0; r <= maxr; ++r) {
-                    if (act && rank == r) apply_posting(ps[u].j, ps[u].v, xs[u], xrs[u], xl);
+                    if (act && rk[u] == r) apply_posting(ps[u].j, ps[u].v, xs[u], xrs[u], xl);
                     __syncwarp();
                   }
                 } else {

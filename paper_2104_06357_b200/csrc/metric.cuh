@@ -152,6 +152,15 @@ template <int CK, typename T>
 __device__ __forceinline__ T contrib(T a, T b, T p) {
   if constexpr (CK == C_MUL) {
     return mul_rn(a, b);
+  } else if constexpr (CK == C_KL && sizeof(T) == 4) {
+    // fp32 fused path: the quotient by the fast reciprocal-multiply division
+    // (<= 2 ulp; the log of the rounded quotient is off by ~u_T absolutely
+    // either way, which the parity rule's KL slack allows), huge divisors
+    // pre-scaled into the approximate divide's range
+    if (!(a > T(0))) return T(0);
+    const T y = b > T(0) ? b : T(1);
+    const T sc = y > T(1e30) ? T(0x1p-64) : T(1);
+    return mul_rn(a, log_(__fdividef(a * sc, y * sc)));
   } else if constexpr (CK == C_KL) {
     return product<SD_SR_KL_TERM, T>(a, b, p);
   } else if constexpr (CK == C_MAX) {
