@@ -29,4 +29,6 @@ if [ -z "$SKIP_NCU" ]; then
   timeout 120 python tools/hbm_probe.py > gpurun_out/hbm_probe.json 2>&1
 fi
 for m in cosine manhattan; do timeout 300 python tools/timeline.py --metric $m 2>/dev/null | grep -v "^ *[0-9.]* *[0-9.]* *[0-9.]* *[0-9]* *step$" > gpurun_out/timeline_c2_$m.txt; done
+timeout 300 python tools/timeline.py --metric cosine --queries 1250 2>/dev/null | grep -v "^ *[0-9.]* *[0-9.]* *[0-9.]* *[0-9]* *step$" > gpurun_out/timeline_c2_cosine_q1250.txt
+timeout 300 python tools/timeline.py --workload c5 --steps 2 2>/dev/null | grep -v "^ *[0-9.]* *[0-9.]* *[0-9.]* *[0-9]* *step$" > gpurun_out/timeline_c5_cosine.txt
 ls gpurun_out | wc -l

@@ -71,7 +71,8 @@ def main(tag):
         keep = [l for l in lines if l.startswith("ok ") or "SUMMARY" in l]
         hdr = f"# compute-sanitizer --tool {tool} (tools/sanitize.sh -> python tools/sanitize_cases.py)\n"
         open(os.path.join(PROF, f"{tag}_sanitize_{tool}.txt"), "w").write(hdr + "\n".join(keep) + "\n")
-    for name in ("hbm_probe.json", "timeline_c2_cosine.txt", "timeline_c2_manhattan.txt"):
+    for name in ("hbm_probe.json", "timeline_c2_cosine.txt", "timeline_c2_manhattan.txt",
+                 "timeline_c2_cosine_q1250.txt", "timeline_c5_cosine.txt"):
         f = os.path.join(OUT, name)
         if os.path.exists(f):
             open(os.path.join(PROF, f"{tag}_{name}"), "w").write(open(f).read())
