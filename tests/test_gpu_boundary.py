@@ -619,3 +619,19 @@ def test_integration_md_binding():
         assert_parity(got, O.pairwise_distances(a, b, name), a, b, name, np.float64, what="INTEGRATION")
     with pytest.raises(sd.DimensionMismatch):
         ns["pairwise_distances_gpu"](a, sd.from_dense(np.ones((2, 3))), sd.metric_registry("cosine"))
+
+
+# ------------------------------------------------------------ CSR -> COO on device (sparse.py:220-225)
+
+@pytest.mark.parametrize("shape", [(0, 5, 0.0), (7, 9, 0.0), (64, 300, 0.05), (513, 2000, 0.02)])
+def test_csr_to_coo_device_matches_host(shape):
+    """sd_csr_to_coo (coo_rows_kernel) against the reference's row expansion
+    (np.repeat over the row degrees), empty rows and empty matrices included."""
+    from paper_2104_06357_b200 import _lib
+    m, k, dens = shape
+    rng = np.random.default_rng(m + k)
+    a = sd.from_dense(_random_dense(rng, m, k, dens)) if m else sd.from_dense(np.zeros((0, k)))
+    d = sd.to_device(a, "float32")
+    got = _lib.coo_rows(d).cpu().numpy()
+    np.testing.assert_array_equal(got, np.asarray(a.coo_row_ids))
+    np.testing.assert_array_equal(np.asarray(sd.csr_to_coo(a).rows), got)

@@ -25,7 +25,7 @@ if [ -z "$SKIP_NCU" ]; then
   for k in dense_tc hgather heavy_rows; do NCU_SPECS=c2:cosine NCU_KERNEL=$k bash tools/gpu_ncu.sh; done
   for k in hminsum hgather; do NCU_SPECS=c2:manhattan NCU_KERNEL=$k bash tools/gpu_ncu.sh; done
   NCU_SPECS="c4:hellinger c4:jaccard" NCU_KERNEL=dense_tc bash tools/gpu_ncu.sh
-  bash tools/sanitize.sh
+  # compute-sanitizer is closed on this pool since r02e (runs under it left GPUs needing a reset); last logs: profiles/r02d_sanitize_*.txt
   timeout 120 python tools/hbm_probe.py > gpurun_out/hbm_probe.json 2>&1
 fi
 for m in cosine manhattan; do timeout 300 python tools/timeline.py --metric $m 2>/dev/null | grep -v "^ *[0-9.]* *[0-9.]* *[0-9.]* *[0-9]* *step$" > gpurun_out/timeline_c2_$m.txt; done
