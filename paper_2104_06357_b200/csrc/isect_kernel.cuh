@@ -195,6 +195,44 @@ __device__ __forceinline__ void sts4_zero(uint32_t a, double) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a + 16), "d"(0.0) : "memory");
 }
 
+// A lane's 4 cells of a 128-cell group in the straight-line epilogue.  fp32:
+// cells 4l..4l+3, one 16-byte access.  fp64: cells 2l, 2l+1, 64+2l, 65+2l —
+// two 16-byte accesses, each contiguous over the warp (512 B: 4 wavefronts,
+// no bank conflicts; with cells 4l..4l+3 a lane's two halves sat 32 B apart
+// and every fp64 epilogue access took twice its wavefronts, r02e ncu: 2.3e8
+// excess shared wavefronts per C2 launch).  Output and statistic rows use the
+// same cells, so the global stores stay fully coalesced too.
+template <typename T> struct EQ;
+template <> struct EQ<float> {
+  static constexpr int CELL = 4;
+  __device__ __forceinline__ static int cell(int lane, int u) { return 4 * lane + u; }
+  __device__ __forceinline__ static void lds(uint32_t a, float* v) { lds4(a, v); }
+  __device__ __forceinline__ static void sts_zero(uint32_t a) { sts4_zero(a, 0.f); }
+  __device__ __forceinline__ static void ldg(const float* p, float* v) { V4<float>::load(p, v); }
+  __device__ __forceinline__ static void stg(float* p, const float* v) { V4<float>::store(p, v); }
+};
+template <> struct EQ<double> {
+  static constexpr int CELL = 2;
+  __device__ __forceinline__ static int cell(int lane, int u) { return 2 * lane + (u & 1) + (u >> 1) * 64; }
+  __device__ __forceinline__ static void lds(uint32_t a, double* v) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a) : "memory");
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 512u) : "memory");
+  }
+  __device__ __forceinline__ static void sts_zero(uint32_t a) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a), "d"(0.0) : "memory");
+    asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a + 512u), "d"(0.0) : "memory");
+  }
+  __device__ __forceinline__ static void ldg(const double* p, double* v) {
+    const double2 x = *reinterpret_cast<const double2*>(p);
+    const double2 y = *reinterpret_cast<const double2*>(p + 64);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+  }
+  __device__ __forceinline__ static void stg(double* p, const double* v) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    __stcs(reinterpret_cast<double2*>(p + 64), make_double2(v[2], v[3]));
+  }
+};
+
 // Metrics whose value for a cell without any intersecting column is a
 // per-query constant once the query row is non-empty (the common case on
 // sparse data): the epilogue then skips the division entirely.
@@ -559,20 +597,21 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
           auto run = [&](auto nz) {
             constexpr int NZM = decltype(nz)::value;
             constexpr bool NZ = NZM > 0;
-            T* op = KPL == 0 ? a.out + i * a.ldo + j0 + 4 * lane : nullptr;
-            const T* p0 = SB0 ? a.sb0 + j0 + 4 * lane : nullptr;
-            const T* p1 = SB1 ? a.sb1 + j0 + 4 * lane : nullptr;
-            uint32_t sa = acc_s + 4u * uint32_t(lane) * ES;
-            uint32_t sc = cnt_s + 4u * uint32_t(lane) * ES;
+            constexpr int LC = EQ<T>::CELL;  // the lane's first cell of a group: LC * lane
+            T* op = KPL == 0 ? a.out + i * a.ldo + j0 + LC * lane : nullptr;
+            const T* p0 = SB0 ? a.sb0 + j0 + LC * lane : nullptr;
+            const T* p1 = SB1 ? a.sb1 + j0 + LC * lane : nullptr;
+            uint32_t sa = acc_s + uint32_t(LC) * uint32_t(lane) * ES;
+            uint32_t sc = cnt_s + uint32_t(LC) * uint32_t(lane) * ES;
             // EPF register sets: group g is finished while the next EPF-1
             // groups' shared and global loads are in flight
             T gv[EPF][4], gc[EPF][4], g0[EPF][4], g1[EPF][4];
             auto load = [&](uint32_t off, T* v, T* c, T* b0, T* b1) {
-              lds4(sa + off * ES, v);
-              sts4_zero(sa + off * ES, T(0));
-              if constexpr (KL) { lds4(sc + off * ES, c); sts4_zero(sc + off * ES, T(0)); }
-              if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) V4<T>::load(p0 + off, b0);
-              if constexpr (SB1 && NZM != 2) V4<T>::load(p1 + off, b1);
+              EQ<T>::lds(sa + off * ES, v);
+              EQ<T>::sts_zero(sa + off * ES);
+              if constexpr (KL) { EQ<T>::lds(sc + off * ES, c); EQ<T>::sts_zero(sc + off * ES); }
+              if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) EQ<T>::ldg(p0 + off, b0);
+              if constexpr (SB1 && NZM != 2) EQ<T>::ldg(p1 + off, b1);
             };
             auto finish = [&](uint32_t off, const T* v, const T* c, const T* b0, const T* b1) {
               T r[4];
@@ -600,10 +639,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                 }
                 if (__any_sync(FULL, poss)) {
 #pragma unroll
-                  for (int u = 0; u < 4; ++u) top.offer(ok[u], r[u], j0 + off + 4 * lane + u, a.topk);
+                  for (int u = 0; u < 4; ++u) top.offer(ok[u], r[u], j0 + off + EQ<T>::cell(lane, u), a.topk);
                 }
               } else {
-                V4<T>::store(op + off, r);
+                EQ<T>::stg(op + off, r);
               }
             };
 #pragma unroll
