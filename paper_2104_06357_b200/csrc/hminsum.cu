@@ -211,7 +211,9 @@ __global__ void __launch_bounds__((MS_WARPS + 1) * 32, 1) hminsum_kernel(
     const int64_t i = k - k0;
     const int s = int(i % MS_STAGES);
     mbar_wait(fb + 8 * s, uint32_t((i / MS_STAGES) & 1));
-    const uint32_t sq = sbase + uint32_t(s) * MS_STAGE_BYTES + uint32_t(lane) * 4u * uint32_t(sizeof(T));
+    // the lane's 4 queries: 4l..4l+3 (fp32), 2l, 2l+1, 64+2l, 65+2l (fp64: each
+    // 16-byte shared load contiguous over the warp, EQ<T> in isect_kernel.cuh)
+    const uint32_t sq = sbase + uint32_t(s) * MS_STAGE_BYTES + uint32_t(lane) * uint32_t(EQ<T>::CELL * sizeof(T));
 #pragma unroll
     for (int u = 0; u < MS_RPW; ++u) {
       if (hs[u] < 0) continue;  // warp-uniform
@@ -233,8 +235,8 @@ __global__ void __launch_bounds__((MS_WARPS + 1) * 32, 1) hminsum_kernel(
             const uint4 w = *reinterpret_cast<const uint4*>(row + t + v);  // 16-byte aligned pair
             off[v] = w.x; x[v] = __uint_as_float(w.y);
             off[v + 1] = w.z; x[v + 1] = __uint_as_float(w.w);
-            lds4(sq + off[v], d[v]);
-            lds4(sq + off[v + 1], d[v + 1]);
+            EQ<T>::lds(sq + off[v], d[v]);
+            EQ<T>::lds(sq + off[v + 1], d[v + 1]);
           }
 #pragma unroll
           for (int v = 0; v < NV; ++v) minadd4(acc[u], x[v], d[v]);
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__((MS_WARPS + 1) * 32, 1) hminsum_kernel(
 #pragma unroll
           for (int v = 0; v < MS_UNROLL; ++v) {
             en[v] = row[t + v];
-            lds4(sq + en[v].off, d[v]);
+            EQ<T>::lds(sq + en[v].off, d[v]);
           }
 #pragma unroll
           for (int v = 0; v < MS_UNROLL; ++v) minadd4(acc[u], en[v].v, d[v]);
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__((MS_WARPS + 1) * 32, 1) hminsum_kernel(
           T d[4];
           const uint32_t o = __shfl_sync(0xffffffffu, ol, t);
           const T x = __shfl_sync(0xffffffffu, vl, t);
-          lds4(sq + o, d);
+          EQ<T>::lds(sq + o, d);
           minadd4(acc[u], x, d);
         }
       }
@@ -272,10 +274,18 @@ __global__ void __launch_bounds__((MS_WARPS + 1) * 32, 1) hminsum_kernel(
     __syncwarp();
     if (lane == 0) mbar_arrive(eb + 8 * s);  // this warp is done with stage s
   }
-  T* out = part + g * hpad * qpad + qb * 128 + 4 * lane;
+  T* out = part + g * hpad * qpad + qb * 128 + EQ<T>::CELL * lane;
 #pragma unroll
-  for (int u = 0; u < MS_RPW; ++u)
-    if (hs[u] >= 0) V4<T>::store_plain(out + int64_t(hs[u]) * qpad, acc[u]);
+  for (int u = 0; u < MS_RPW; ++u) {
+    if (hs[u] < 0) continue;
+    T* o = out + int64_t(hs[u]) * qpad;
+    if constexpr (sizeof(T) == 4) {
+      V4<T>::store_plain(o, acc[u]);
+    } else {
+      reinterpret_cast<double2*>(o)[0] = make_double2(acc[u][0], acc[u][1]);
+      reinterpret_cast<double2*>(o + 64)[0] = make_double2(acc[u][2], acc[u][3]);
+    }
+  }
 }
 
 // dqh[q][h] = sum over groups (in order) of part[g][h][q]

@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
     if (it >= total) break;
     const int64_t j = lrows[it / nblk], blk = int64_t(it % nblk);
     const int64_t beg = ptr[j], end = ptr[j + 1];
-    const T* dcol = D + blk * bstride + QPL * lane;
+    // QPL = 4: the lane's queries as in EQ<T> (isect_kernel.cuh) — fp64 loads
+    // and stores contiguous over the warp
+    const T* dcol = D + blk * bstride + (QPL == 4 ? EQ<T>::CELL : 1) * lane;
     T acc[QPL];
 #pragma unroll
     for (int k = 0; k < QPL; ++k) acc[k] = T(0);
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
           const int32_t c = __shfl_sync(0xffffffffu, cl, src);
           x[u] = __shfl_sync(0xffffffffu, vl, src);
           if (u0 + u < nn) {
-            if constexpr (QPL == 4) V4<T>::load(dcol + int64_t(c) * ld, d[u]);
+            if constexpr (QPL == 4) EQ<T>::ldg(dcol + int64_t(c) * ld, d[u]);
             else d[u][0] = dcol[int64_t(c) * ld];
           }
         }
@@ -476,7 +478,13 @@ __global__ void __launch_bounds__(256) hgather_kernel(const int64_t* __restrict_
               acc[k] = MINSUM ? add_rn(acc[k], min_(x[u], d[u][k])) : fma_rn(x[u], d[u][k], acc[k]);
       }
     }
-    if constexpr (QPL == 4) V4<T>::store_plain(out + j * ldo + blk * 128 + 4 * lane, acc);
+    if constexpr (QPL == 4 && sizeof(T) == 4) {
+      V4<T>::store_plain(out + j * ldo + blk * 128 + 4 * lane, acc);
+    } else if constexpr (QPL == 4) {
+      T* o = out + j * ldo + blk * 128 + 2 * lane;
+      reinterpret_cast<double2*>(o)[0] = make_double2(acc[0], acc[1]);
+      reinterpret_cast<double2*>(o + 64)[0] = make_double2(acc[2], acc[3]);
+    }
     else out[j * ldo + blk * 32 + lane] = acc[0];
   }
 }
