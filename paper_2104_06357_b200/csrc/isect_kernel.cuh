@@ -613,7 +613,30 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) EQ<T>::ldg(p0 + off, b0);
               if constexpr (SB1 && NZM != 2) EQ<T>::ldg(p1 + off, b1);
             };
+            T taup = T(0);
+            auto retau = [&]() {
+              if constexpr (KPL > 0 && M == SD_M_COSINE && NZM == 2) {
+                const T thr = top.thr_d;
+                const T E = thr != thr ? gbound : min_(thr, gbound);
+                const T tau = mul_rn(sub_rn(T(1), E), ra0);
+                taup = sub_rn(tau, mul_rn(add_rn(abs_(tau), ra0), T(0x1p-18)));
+              }
+            };
+            retau();
             auto finish = [&](uint32_t off, const T* v, const T* c, const T* b0, const T* b1) {
+              if constexpr (KPL > 0 && M == SD_M_COSINE && NZM == 2) {
+                // kNN cosine over scaled postings: once a group cannot beat
+                // the bound E (the list's k-th distance, or the query's shared
+                // bound), r = 1 - v / ||a|| <= E needs v >= (1 - E) ||a||.  A
+                // group whose every accumulator lies below that threshold,
+                // lowered by a margin far above the rounding of r and of the
+                // threshold itself, is one the exact vote below would reject:
+                // skip its arithmetic (C5: after the lists fill, ~all groups).
+                // NaN accumulators pass to the exact path.
+                // (taup: recomputed per tile and after every offer)
+                const bool pass = !(v[0] < taup) || !(v[1] < taup) || !(v[2] < taup) || !(v[3] < taup);
+                if (!__any_sync(FULL, pass)) return;
+              }
               T r[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -640,6 +663,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                 if (__any_sync(FULL, poss)) {
 #pragma unroll
                   for (int u = 0; u < 4; ++u) top.offer(ok[u], r[u], j0 + off + EQ<T>::cell(lane, u), a.topk);
+                  retau();
                 }
               } else {
                 EQ<T>::stg(op + off, r);
