@@ -202,12 +202,36 @@ __device__ __forceinline__ void sts4_zero(uint32_t a, double) {
 // and every fp64 epilogue access took twice its wavefronts, r02e ncu: 2.3e8
 // excess shared wavefronts per C2 launch).  Output and statistic rows use the
 // same cells, so the global stores stay fully coalesced too.
+// ldz(): read the 4 cells and leave zeros behind.  SD_ISECT_XCHG = 1: one
+// 16-byte shared exchange per half (ATOMS.EXCH.128) instead of a load and a
+// store of zeros (the zeroing stores were 17% of the C2 sweep's LSU wavefronts)
+#ifndef SD_ISECT_XCHG
+#define SD_ISECT_XCHG 0
+#endif
+__device__ __forceinline__ void xchg16_zero(uint32_t a, uint32_t* w) {
+  unsigned long long lo, hi;
+  asm volatile("{\n .reg .b128 z, o;\n mov.b128 z, {%2, %2};\n atom.shared.exch.b128 o, [%3], z;\n"
+               " mov.b128 {%0, %1}, o;\n}"
+               : "=l"(lo), "=l"(hi) : "l"(0ull), "r"(a) : "memory");
+  w[0] = uint32_t(lo); w[1] = uint32_t(lo >> 32); w[2] = uint32_t(hi); w[3] = uint32_t(hi >> 32);
+}
 template <typename T> struct EQ;
 template <> struct EQ<float> {
   static constexpr int CELL = 4;
   __device__ __forceinline__ static int cell(int lane, int u) { return 4 * lane + u; }
   __device__ __forceinline__ static void lds(uint32_t a, float* v) { lds4(a, v); }
   __device__ __forceinline__ static void sts_zero(uint32_t a) { sts4_zero(a, 0.f); }
+  __device__ __forceinline__ static void ldz(uint32_t a, float* v) {
+#if SD_ISECT_XCHG
+    uint32_t w[4];
+    xchg16_zero(a, w);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __uint_as_float(w[u]);
+#else
+    lds(a, v);
+    sts_zero(a);
+#endif
+  }
   __device__ __forceinline__ static void ldg(const float* p, float* v) { V4<float>::load(p, v); }
   __device__ __forceinline__ static void stg(float* p, const float* v) { V4<float>::store(p, v); }
 };
@@ -221,6 +245,20 @@ template <> struct EQ<double> {
   __device__ __forceinline__ static void sts_zero(uint32_t a) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a), "d"(0.0) : "memory");
     asm volatile("st.shared.v2.f64 [%0], {%1, %1};" :: "r"(a + 512u), "d"(0.0) : "memory");
+  }
+  __device__ __forceinline__ static void ldz(uint32_t a, double* v) {
+#if SD_ISECT_XCHG
+    uint32_t w[4];
+    xchg16_zero(a, w);
+    v[0] = __hiloint2double(int(w[1]), int(w[0]));
+    v[1] = __hiloint2double(int(w[3]), int(w[2]));
+    xchg16_zero(a + 512u, w);
+    v[2] = __hiloint2double(int(w[1]), int(w[0]));
+    v[3] = __hiloint2double(int(w[3]), int(w[2]));
+#else
+    lds(a, v);
+    sts_zero(a);
+#endif
   }
   __device__ __forceinline__ static void ldg(const double* p, double* v) {
     const double2 x = *reinterpret_cast<const double2*>(p);
@@ -607,9 +645,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
             // groups' shared and global loads are in flight
             T gv[EPF][4], gc[EPF][4], g0[EPF][4], g1[EPF][4];
             auto load = [&](uint32_t off, T* v, T* c, T* b0, T* b1) {
-              EQ<T>::lds(sa + off * ES, v);
-              EQ<T>::sts_zero(sa + off * ES);
-              if constexpr (KL) { EQ<T>::lds(sc + off * ES, c); EQ<T>::sts_zero(sc + off * ES); }
+              EQ<T>::ldz(sa + off * ES, v);
+              if constexpr (KL) EQ<T>::ldz(sc + off * ES, c);
               if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) EQ<T>::ldg(p0 + off, b0);
               if constexpr (SB1 && NZM != 2) EQ<T>::ldg(p1 + off, b1);
             };
