@@ -446,7 +446,7 @@ int isect_run(const sd_csr* a, const sd_csr* b, const sd_index* ix, int dtype, c
   if (m == 0 || b->n_rows == 0) return SD_OK;
   if (m >= (int64_t(1) << 31)) { set_error("too many query rows"); return SD_E_INVALID; }
   const size_t es = dtype == SD_F64 ? 8 : 4;
-  const int64_t per_warp = int64_t(ix->tile) * int64_t(es) * ((ck == C_KL || ck == C_MAX) ? 2 : 1);
+  const int64_t per_warp = int64_t(ix->tile) * (int64_t(es) + isect_second_bytes(ck, int64_t(es)));
   const bool hyb = isect_hybrid_eligible(ix, md, topk);
   // with the hybrid gather in the sweep's shadow (hybrid.cu) the sweep leaves
   // room for its 128-thread block on every SM: 12 warps (192 KB, 48 K registers)

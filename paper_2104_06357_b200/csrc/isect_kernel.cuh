@@ -202,6 +202,41 @@ __device__ __forceinline__ void sts4_zero(uint32_t a, double) {
 // and every fp64 epilogue access took twice its wavefronts, r02e ncu: 2.3e8
 // excess shared wavefronts per C2 launch).  Output and statistic rows use the
 // same cells, so the global stores stay fully coalesced too.
+// KL coverage counts: 16 bits per cell (a count never exceeds the query
+// row's degree; rows of >= 65,536 columns are settled exactly, kl_count
+// below), so a warp needs TJ x (sizeof(T) + 2) bytes and 9 warps fit an SM
+// instead of 7 (fp64: 11 instead of 7)
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" :: "r"(a), "h"((unsigned short)v) : "memory");
+}
+// 4 consecutive counts (8 bytes), zeroed behind
+template <typename T>
+__device__ __forceinline__ void ldz_cnt4(uint32_t a, T* c) {
+  uint32_t w0, w1;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(a) : "memory");
+  asm volatile("st.shared.v2.u32 [%0], {%1, %1};" :: "r"(a), "r"(0u) : "memory");
+  c[0] = T(w0 & 0xffffu); c[1] = T(w0 >> 16); c[2] = T(w1 & 0xffffu); c[3] = T(w1 >> 16);
+}
+// the counts of a lane's 4 epilogue cells (EQ<T> layout), zeroed behind
+template <typename T>
+__device__ __forceinline__ void ldz_cnt_eq(uint32_t a, T* c) {
+  if constexpr (sizeof(T) == 4) {
+    ldz_cnt4(a, c);
+  } else {
+    uint32_t w0, w1;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(a) : "memory");
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w1) : "r"(a + 128u) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(0u) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" :: "r"(a + 128u), "r"(0u) : "memory");
+    c[0] = T(w0 & 0xffffu); c[1] = T(w0 >> 16); c[2] = T(w1 & 0xffffu); c[3] = T(w1 >> 16);
+  }
+}
+
 // ldz(): read the 4 cells and leave zeros behind.  SD_ISECT_XCHG = 1: one
 // 16-byte shared exchange per half (ATOMS.EXCH.128) instead of a load and a
 // store of zeros (the zeroing stores were 17% of the C2 sweep's LSU wavefronts)
@@ -335,6 +370,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
   constexpr int CK = metric_contrib(M);
   constexpr bool MX = CK == C_MAX;
   constexpr bool KL = CK == C_KL || MX;   // second per-cell array: KL counts / chebyshev masks
+  constexpr bool KC = CK == C_KL;         // ... of 16-bit KL counts
   constexpr bool SB0 = (M == SD_M_CORRELATION || M == SD_M_COSINE || M == SD_M_DICE || M == SD_M_EUCLIDEAN ||
                         M == SD_M_JACCARD || is_namm(M));
   constexpr bool SB1 = M == SD_M_CORRELATION || M == SD_M_COSINE;
@@ -352,11 +388,12 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
   const int lane = threadIdx.x & 31;
   const int TJ = a.tile;
   constexpr uint32_t ES = sizeof(T);
+  constexpr uint32_t CS = KC ? 2u : (MX ? ES : 0u);  // bytes per cell of the second array
   // opaque copies: keeps the accumulator base and the posting pointer in
   // registers instead of letting the compiler rebuild them per access
   uint32_t acc_s;
   asm volatile("mov.b32 %0, %1;" : "=r"(acc_s)
-               : "r"(uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(warp) * TJ * ES * (KL ? 2u : 1u)));
+               : "r"(uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(warp) * TJ * (ES + CS)));
   const uint32_t cnt_s = acc_s + uint32_t(TJ) * ES;
   const Posting<T>* __restrict__ post = a.post;
   const uint64_t l2pol = l2_evict_last_policy();
@@ -386,13 +423,14 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
       if constexpr (CK == C_JS) c = js_contrib(x, xl, bv);  // log(x) once per column
       else c = contrib<CK, T>(x, bv, p);
       sts(ad, add_rn(lds(ad, T(0)), c));
-      if constexpr (KL) sts(cnt_s + jr * ES, add_rn(lds(cnt_s + jr * ES, T(0)), T(1)));
+      if constexpr (KC) sts_u16(cnt_s + jr * 2u, lds_u16(cnt_s + jr * 2u) + 1u);
     }
   };
 
   for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
     sts(acc_s + q * ES, T(0));
-    if constexpr (KL) sts(cnt_s + q * ES, T(0));
+    if constexpr (KC) sts_u16(cnt_s + q * 2u, 0u);
+    else if constexpr (MX) sts(cnt_s + q * ES, T(0));
   }
   __syncwarp();
 
@@ -420,6 +458,22 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
     if (a.skip && a.skip[i] >= 0) continue;
     const int64_t abeg = a.a_ptr[i], aend = a.a_ptr[i + 1];
     const T ra0 = a.sa0 ? a.sa0[i] : T(0);
+    // KL with a query row of >= 65,536 columns: the 16-bit counts wrap, so a
+    // cell is covered only if B_j holds at least as many columns, the count
+    // agrees modulo 2^16, and a merge of the two sorted rows confirms it
+    const bool kl_big = KC && aend - abeg >= 65536;
+    auto kl_count = [&](T c16, int64_t j) -> T {
+      const int64_t da = aend - abeg, bb = a.b_ptr[j], be = a.b_ptr[j + 1];
+      if (be - bb < da || uint32_t(c16) != uint32_t(da & 0xffff)) return T(0);  // != ra0 (>= 65,536)
+      int64_t ia = abeg, ib = bb, hit = 0;
+      while (ia < aend && ib < be) {
+        const int32_t ca = a.a_idx[ia], cb = a.b_idx[ib];
+        hit += ca == cb;
+        ia += ca <= cb;
+        ib += cb <= ca;
+      }
+      return T(hit);
+    };
     const T ra1 = a.sa1 ? a.sa1[i] : T(0);
     T topa_l = T(0);  // chebyshev: lane r holds the r-th largest |a| of the query row
     if constexpr (MX) topa_l = lane < CHEB_K ? a.topa[int64_t(lane) * a.m + i] : T(0);
@@ -640,13 +694,14 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
             const T* p0 = SB0 ? a.sb0 + j0 + LC * lane : nullptr;
             const T* p1 = SB1 ? a.sb1 + j0 + LC * lane : nullptr;
             uint32_t sa = acc_s + uint32_t(LC) * uint32_t(lane) * ES;
-            uint32_t sc = cnt_s + uint32_t(LC) * uint32_t(lane) * ES;
+            uint32_t sc = cnt_s + uint32_t(LC) * uint32_t(lane) * CS;
             // EPF register sets: group g is finished while the next EPF-1
             // groups' shared and global loads are in flight
             T gv[EPF][4], gc[EPF][4], g0[EPF][4], g1[EPF][4];
             auto load = [&](uint32_t off, T* v, T* c, T* b0, T* b1) {
               EQ<T>::ldz(sa + off * ES, v);
-              if constexpr (KL) EQ<T>::ldz(sc + off * ES, c);
+              if constexpr (KC) ldz_cnt_eq<T>(sc + off * CS, c);
+              else if constexpr (KL) EQ<T>::ldz(sc + off * ES, c);
               if constexpr (SB0 && !(M == SD_M_COSINE && NZ)) EQ<T>::ldg(p0 + off, b0);
               if constexpr (SB1 && NZM != 2) EQ<T>::ldg(p1 + off, b1);
             };
@@ -674,6 +729,14 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                 const bool pass = !(v[0] < taup) || !(v[1] < taup) || !(v[2] < taup) || !(v[3] < taup);
                 if (!__any_sync(FULL, pass)) return;
               }
+              T cc[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) cc[u] = KL ? c[u] : T(0);
+              if constexpr (KC) {
+                if (kl_big)
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) cc[u] = kl_count(cc[u], j0 + off + EQ<T>::cell(lane, u));
+              }
               T r[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -683,7 +746,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
                   r[u] = sub_rn(T(1), mul_rn(v[u], mul_rn(ra1, b1[u])));
                 } else {
                   uint32_t f = 0;
-                  r[u] = isect_cell<T, M>(a, v[u], KL ? c[u] : T(0), ra0, ra1, SB0 ? b0[u] : T(0),
+                  r[u] = isect_cell<T, M>(a, v[u], cc[u], ra0, ra1, SB0 ? b0[u] : T(0),
                                           SB1 ? b1[u] : T(0), fast_zero, zero_val, f);
                   flags |= f;
                 }
@@ -738,7 +801,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         if (q + 3 < nt) {
           lds4(acc_s + q * ES, gv);
           sts4_zero(acc_s + q * ES, T(0));
-          if constexpr (KL) { lds4(cnt_s + q * ES, gcv); sts4_zero(cnt_s + q * ES, T(0)); }
+          if constexpr (KC) ldz_cnt4<T>(cnt_s + q * CS, gcv);
+          else if constexpr (KL) { lds4(cnt_s + q * ES, gcv); sts4_zero(cnt_s + q * ES, T(0)); }
           if constexpr (SB0) { if (need_sb0) V4<T>::load(a.sb0 + j0 + q, gb0); }
           if constexpr (SB1) { if (need_sb1) V4<T>::load(a.sb1 + j0 + q, gb1); }
         } else {
@@ -747,7 +811,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
             if (q + u < nt) {
               gv[u] = lds(acc_s + (q + u) * ES, T(0));
               sts(acc_s + (q + u) * ES, T(0));
-              if constexpr (KL) { gcv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
+              if constexpr (KC) { gcv[u] = T(lds_u16(cnt_s + (q + u) * CS)); sts_u16(cnt_s + (q + u) * CS, 0u); }
+              else if constexpr (KL) { gcv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
               if constexpr (SB0) { if (need_sb0) gb0[u] = a.sb0[j0 + q + u]; }
               if constexpr (SB1) { if (need_sb1) gb1[u] = a.sb1[j0 + q + u]; }
             }
@@ -796,7 +861,9 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             uint32_t f = 0;
-            r[u] = isect_cell<T, M>(a, gv[u], gcv[u], ra0, ra1, gb0[u], gb1[u], fast_zero, zero_val, f);
+            T cu = gcv[u];
+            if constexpr (KC) { if (kl_big && q + u < nt) cu = kl_count(cu, j0 + q + u); }
+            r[u] = isect_cell<T, M>(a, gv[u], cu, ra0, ra1, gb0[u], gb1[u], fast_zero, zero_val, f);
             if (q + u < nt) flags |= f;  // lanes past the tile end evaluate a dummy cell
           }
         }
@@ -1015,8 +1082,7 @@ int launch_heavy_rows(IsectArgs<T>& a, const int32_t* hq, int nhq, const int32_t
 
 template <typename T, int M, int KPL>
 int launch_isect_kernel(IsectArgs<T>& args, int W, cudaStream_t st) {
-  const int64_t per_warp = int64_t(args.tile) * sizeof(T) *
-                           ((metric_contrib(M) == C_KL || metric_contrib(M) == C_MAX) ? 2 : 1);
+  const int64_t per_warp = int64_t(args.tile) * (int64_t(sizeof(T)) + isect_second_bytes(metric_contrib(M), sizeof(T)));
   const size_t smem = size_t(W) * per_warp;
   SD_TRY(prepare_smem(isect_kernel<T, M, KPL>, smem, "isect_kernel"));
   int per_sm = 0;

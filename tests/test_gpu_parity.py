@@ -581,3 +581,33 @@ def test_timings_report_device_footprint():
     assert timings["device_index_bytes"] > 0
     assert timings["device_output_bytes"] >= 30 * 50 * 4
     assert report.peak_accumulator_entries >= 0
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_kl_coverage_rows_over_65536_columns(dtype):
+    """The fused kernel keeps 16-bit KL coverage counts; query rows of >= 65,536
+    columns are settled by the index row's degree, the count modulo 2^16 and a
+    merge of the sorted rows (metrics.py:352-366 coverage, permissive KL)."""
+    n = 140000
+    rng = np.random.default_rng(65536)
+
+    def rows(col_sets):
+        d = np.zeros((len(col_sets), n))
+        for r, cols in enumerate(col_sets):
+            d[r, cols] = rng.uniform(0.1, 1.0, len(cols))
+        return sd.from_dense(d)
+
+    q = rows([np.arange(66000), np.arange(65536), np.arange(0, 40, 4)])
+    b = rows([np.arange(70000),                       # covers all three queries
+              np.arange(1, 66001),                    # misses column 0
+              np.arange(70000, 136000),               # disjoint from query 1 (count 0 == 65536 mod 2^16)
+              np.arange(0, 65999),                    # one column short of query 0
+              np.arange(0, 40, 2)])                   # covers query 2 only
+    got = sd.pairwise_distances(q, b, sd.metric_registry("kl", strict=False), dtype=dtype)
+    ref = O.pairwise_distances_c(q, b, "kl", strict=False)
+    covered = ref < 1e300
+    assert covered.tolist() == [[True, False, False, False, False],
+                                [True, False, False, True, False],
+                                [True, False, False, True, True]]
+    assert (np.isfinite(got) & (got < 1e300)).tolist() == covered.tolist()
+    assert_parity(got, ref, q, b, "kl", dtype, what="kl rows over 65,536 columns")
