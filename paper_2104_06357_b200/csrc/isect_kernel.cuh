@@ -77,11 +77,6 @@ struct IsectArgs {
   typename OrdKey<T>::type* kth;
 };
 
-// chebyshev hit masks live in the second accumulator array as raw bits
-__device__ __forceinline__ uint32_t to_mask(float v) { return __float_as_uint(v); }
-__device__ __forceinline__ uint32_t to_mask(double v) { return uint32_t(v); }
-__device__ __forceinline__ float from_mask(uint32_t m, float) { return __uint_as_float(m); }
-__device__ __forceinline__ double from_mask(uint32_t m, double) { return double(m); }
 
 // fast epilogue: 128-cell groups in flight per warp
 #ifndef SD_ISECT_EPF
@@ -388,7 +383,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
   const int lane = threadIdx.x & 31;
   const int TJ = a.tile;
   constexpr uint32_t ES = sizeof(T);
-  constexpr uint32_t CS = KC ? 2u : (MX ? ES : 0u);  // bytes per cell of the second array
+  constexpr uint32_t CS = (KC || MX) ? 2u : 0u;  // bytes per cell of the second array (16-bit)
+  // chebyshev hit masks: the top-MK ranks of each side (bits 0..7 the query
+  // row's, 8..15 the index row's); the index keeps ranks up to CHEB_K
+  constexpr int MK = 8;
   // opaque copies: keeps the accumulator base and the posting pointer in
   // registers instead of letting the compiler rebuild them per access
   uint32_t acc_s;
@@ -412,10 +410,10 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
       const T m = contrib<CK, T>(x, bv, p);
       const T old = lds(ad, T(0));
       sts(ad, m > old ? m : old);
-      const uint32_t bits = (xr < CHEB_K ? (1u << xr) : 0u) | (rb < CHEB_K ? (1u << (16 + rb)) : 0u);
+      const uint32_t bits = (xr < MK ? (1u << xr) : 0u) | (rb < MK ? (1u << (8 + rb)) : 0u);
       if (bits) {
-        const uint32_t am = cnt_s + jl * ES;
-        sts(am, from_mask(to_mask(lds(am, T(0))) | bits, T(0)));
+        const uint32_t am = cnt_s + jl * 2u;
+        sts_u16(am, lds_u16(am) | bits);
       }
     } else {
       const uint32_t ad = acc_s + jr * ES;
@@ -429,8 +427,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
 
   for (int q = lane; q < TJ; q += 32) {  // accumulators start zeroed; the epilogue re-zeroes
     sts(acc_s + q * ES, T(0));
-    if constexpr (KC) sts_u16(cnt_s + q * 2u, 0u);
-    else if constexpr (MX) sts(cnt_s + q * ES, T(0));
+    if constexpr (KC || MX) sts_u16(cnt_s + q * 2u, 0u);
   }
   __syncwarp();
 
@@ -801,7 +798,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         if (q + 3 < nt) {
           lds4(acc_s + q * ES, gv);
           sts4_zero(acc_s + q * ES, T(0));
-          if constexpr (KC) ldz_cnt4<T>(cnt_s + q * CS, gcv);
+          if constexpr (KC || MX) ldz_cnt4<T>(cnt_s + q * CS, gcv);
           else if constexpr (KL) { lds4(cnt_s + q * ES, gcv); sts4_zero(cnt_s + q * ES, T(0)); }
           if constexpr (SB0) { if (need_sb0) V4<T>::load(a.sb0 + j0 + q, gb0); }
           if constexpr (SB1) { if (need_sb1) V4<T>::load(a.sb1 + j0 + q, gb1); }
@@ -811,7 +808,7 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
             if (q + u < nt) {
               gv[u] = lds(acc_s + (q + u) * ES, T(0));
               sts(acc_s + (q + u) * ES, T(0));
-              if constexpr (KC) { gcv[u] = T(lds_u16(cnt_s + (q + u) * CS)); sts_u16(cnt_s + (q + u) * CS, 0u); }
+              if constexpr (KC || MX) { gcv[u] = T(lds_u16(cnt_s + (q + u) * CS)); sts_u16(cnt_s + (q + u) * CS, 0u); }
               else if constexpr (KL) { gcv[u] = lds(cnt_s + (q + u) * ES, T(0)); sts(cnt_s + (q + u) * ES, T(0)); }
               if constexpr (SB0) { if (need_sb0) gb0[u] = a.sb0[j0 + q + u]; }
               if constexpr (SB1) { if (need_sb1) gb1[u] = a.sb1[j0 + q + u]; }
@@ -826,16 +823,16 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         if constexpr (MX) {  // max(M_isect, largest |a| not hit, largest |b| not hit)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const uint32_t mk = to_mask(gcv[u]);
-            const int fa = __ffs(~(mk & 0xffffu)) - 1;            // first unhit A rank, 16 = all hit
-            const int fb = __ffs(~(mk >> 16)) - 1;
+            const uint32_t mk = uint32_t(gcv[u]);                 // 16-bit mask, held as a number
+            const int fa = __ffs(~(mk & 0xffu)) - 1;              // first unhit A rank, MK = all hit
+            const int fb = __ffs(~(mk >> 8)) - 1;
             const T ma = __shfl_sync(FULL, topa_l, fa & 31);
             const int64_t j = j0 + q + u;
             T mb = gb0[u];                                         // rank 0 of B row j
-            bool exact = fa == CHEB_K && aend - abeg > CHEB_K;
+            bool exact = fa == MK && aend - abeg > MK;
             if (q + u < nt && fb > 0) {
-              if (fb < CHEB_K) mb = a.topb[int64_t(fb) * a.n + j];
-              else if (a.b_ptr[j + 1] - a.b_ptr[j] > CHEB_K) exact = true;
+              if (fb < MK) mb = a.topb[int64_t(fb) * a.n + j];
+              else if (a.b_ptr[j + 1] - a.b_ptr[j] > MK) exact = true;
               else mb = T(0);
             }
             if (exact && q + u < nt) {  // every top-K entry intersects: exact sorted merge (rare)

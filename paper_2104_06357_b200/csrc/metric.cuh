@@ -137,9 +137,10 @@ __host__ __device__ constexpr int metric_contrib(int metric) {
 }
 
 // bytes per accumulator cell of the fused kernel's second array: 16-bit KL
-// coverage counts, chebyshev hit masks as wide as the value type, none else
+// coverage counts, 16-bit chebyshev hit masks (top-8 ranks of each side),
+// none else
 __host__ __device__ constexpr int64_t isect_second_bytes(int ck, int64_t es) {
-  return ck == C_KL ? 2 : ck == C_MAX ? es : 0;
+  return (ck == C_KL || ck == C_MAX) ? 2 : 0;
 }
 
 __host__ __device__ inline int contrib_semiring(int ck) {
