@@ -18,7 +18,7 @@
 //     values of a chunk, HQT+[c0:c0+CW][128 queries], are one contiguous 64 KB
 //     block (HQT is stored in 128-query blocks) moved into shared memory by a
 //     single bulk copy (TMA engine) on an mbarrier, three stages in flight;
-//   * a CTA owns 64 heavy index rows (16 warps x 4, a stratified sample of
+//   * a CTA owns 60 heavy index rows (20 warps x 3, a stratified sample of
 //     the degree-ordered heavy ids so CTAs and warps carry similar work) and a
 //     group of consecutive chunks (their per-(row, chunk) CSR offsets, hchunk,
 //     built once per index, staged in shared memory); for each chunk a warp
@@ -45,11 +45,23 @@ namespace {
 constexpr int MS_STAGE_BYTES = 65536;
 template <typename T>
 constexpr int ms_stages() { return sizeof(T) == 4 ? 3 : 2; }  // fp64: its staging area needs the room
-constexpr int MS_WARPS = 16;
-constexpr int MS_RPW = 4;                  // heavy rows per warp
+#ifndef SD_MS_WARPS
+#define SD_MS_WARPS 20
+#endif
+#ifndef SD_MS_RPW
+#define SD_MS_RPW 3
+#endif
+#ifndef SD_MS_UNROLL
+#define SD_MS_UNROLL 8
+#endif
+// 20 consumer warps x 3 rows: the block is latency-bound on its shared loads,
+// so more warps beat more rows per warp (C2 fp32 583 -> 527 us; measured
+// 16 x 4, 20 x 3, 22 x 3, 31 x 2: 583 / 527 / 544 / 553 us)
+constexpr int MS_WARPS = SD_MS_WARPS;      // consumer warps (plus one producer warp)
+constexpr int MS_RPW = SD_MS_RPW;          // heavy rows per warp
 constexpr int MS_HB = MS_WARPS * MS_RPW;   // heavy rows per CTA
-constexpr int MS_UNROLL = 8;               // staged entries per step (rows padded to a multiple)
-constexpr int MS_MAX_G = 32;               // chunks per CTA (their pointers: 64 x 33 x 8 B of shared memory)
+constexpr int MS_UNROLL = SD_MS_UNROLL;    // staged entries per step (rows padded to a multiple)
+constexpr int MS_MAX_G = 32;               // chunks per CTA (their pointers: MS_HB x 33 x 8 B of shared memory)
 
 template <typename T>
 constexpr int ms_cw() { return MS_STAGE_BYTES / (128 * int(sizeof(T))); }
@@ -107,7 +119,7 @@ __global__ void not_nonneg_kernel(const T* __restrict__ v, int64_t n, unsigned i
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
-// grid (ceil(nh / 64), groups, qpad / 128); 512 threads; dynamic shared
+// grid (ceil(nh / MS_HB), groups, qpad / 128); (MS_WARPS + 1) x 32 threads; dynamic shared
 // memory ms_stages x 64 KB + the CTA's chunk pointers + per-warp entry staging.  D = HQT+ in 128-query
 // blocks: block qb's column c values at D + (qb * n_cols + c) * 128.  CTA b
 // takes the degree-ordered heavy positions b, b + hblocks, b + 2 hblocks, ...
