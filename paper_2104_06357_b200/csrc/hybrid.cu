@@ -418,15 +418,17 @@ __global__ void hreduce_kernel(const T* __restrict__ P, int splits, int64_t coun
   }
 }
 
-// dense rows in flight per lane in the gather
+// dense rows in flight per lane in the gather (4: fewer registers, more
+// resident warps — C2 cosine 1.98 -> 1.96 ms, C5 18.29 -> 17.94 ms against 8;
+// 16 loses: 2.20 / 20.2 ms)
 #ifndef SD_HGATHER_UNROLL
-#define SD_HGATHER_UNROLL 8
+#define SD_HGATHER_UNROLL 4
 #endif
 constexpr int HGU = SD_HGATHER_UNROLL;
 
 // DLH[j][q] = sum_c b_jc * HQT[c][q] (MINSUM: sum_c min(b_jc, HQT[c][q]))
 // over light index rows j (heavy rows are the dense block's); one warp per
-// (row, 128-wide block of heavy queries), ascending column order, 8 dense
+// (row, 128-wide block of heavy queries), ascending column order, HGU dense
 // rows in flight per lane; the block's values of column c are at
 // D + blk * bstride + c * ld.  Rows are taken from a shared counter in
 // descending-degree order (lrows, index build) so the long rows start first
