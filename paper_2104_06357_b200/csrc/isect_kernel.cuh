@@ -83,6 +83,13 @@ struct IsectArgs {
 #define SD_ISECT_EPF 4
 #endif
 constexpr int EPF = SD_ISECT_EPF;
+// kNN: its groups are voted, not stored — fewer in flight leaves registers to
+// the top-k lists (C5 17.9 -> 16.5 ms with 2; pairwise keeps 4: manhattan
+// 2.72 -> 3.49 ms with 2, and 8 loses everywhere)
+#ifndef SD_ISECT_EPF_KNN
+#define SD_ISECT_EPF_KNN 2
+#endif
+constexpr int EPF_KNN = SD_ISECT_EPF_KNN;
 
 // warps per CTA (one CTA per SM: 14 x 16 KB accumulators = 224 KB); capping
 // the CTA at 448 threads (4 warps on some SM sub-partitions) caps each thread at 128 registers
@@ -680,7 +687,8 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         // straight-line epilogue with pointers advanced per group, no bounds
         // tests, and the per-query cosine branch hoisted out of the cell loop;
         // kNN votes each group against its bounds instead of storing it
-        if ((KPL > 0 || vec_out) && nt == TJ && TJ % (EPF * 128) == 0) {
+        constexpr int EP = KPL > 0 ? EPF_KNN : EPF;  // 128-cell groups in flight
+        if ((KPL > 0 || vec_out) && nt == TJ && TJ % (EP * 128) == 0) {
           // nz: 0 generic cell, 1 cosine of a non-empty query, 2 the same over
           // scaled postings (no per-cell index statistic at all)
           auto run = [&](auto nz) {
@@ -692,9 +700,9 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
             const T* p1 = SB1 ? a.sb1 + j0 + LC * lane : nullptr;
             uint32_t sa = acc_s + uint32_t(LC) * uint32_t(lane) * ES;
             uint32_t sc = cnt_s + uint32_t(LC) * uint32_t(lane) * CS;
-            // EPF register sets: group g is finished while the next EPF-1
+            // EP register sets: group g is finished while the next EP-1
             // groups' shared and global loads are in flight
-            T gv[EPF][4], gc[EPF][4], g0[EPF][4], g1[EPF][4];
+            T gv[EP][4], gc[EP][4], g0[EP][4], g1[EP][4];
             auto load = [&](uint32_t off, T* v, T* c, T* b0, T* b1) {
               EQ<T>::ldz(sa + off * ES, v);
               if constexpr (KC) ldz_cnt_eq<T>(sc + off * CS, c);
@@ -767,14 +775,14 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
               }
             };
 #pragma unroll
-            for (int q = 0; q < EPF; ++q) load(uint32_t(q) * 128u, gv[q], gc[q], g0[q], g1[q]);
+            for (int q = 0; q < EP; ++q) load(uint32_t(q) * 128u, gv[q], gc[q], g0[q], g1[q]);
 #pragma unroll 1
-            for (uint32_t g = 0; g < uint32_t(TJ); g += EPF * 128) {
+            for (uint32_t g = 0; g < uint32_t(TJ); g += EP * 128) {
 #pragma unroll
-              for (int q = 0; q < EPF; ++q) {
+              for (int q = 0; q < EP; ++q) {
                 finish(g + uint32_t(q) * 128u, gv[q], gc[q], g0[q], g1[q]);
-                if (g + uint32_t(q + EPF) * 128u < uint32_t(TJ))
-                  load(g + uint32_t(q + EPF) * 128u, gv[q], gc[q], g0[q], g1[q]);
+                if (g + uint32_t(q + EP) * 128u < uint32_t(TJ))
+                  load(g + uint32_t(q + EP) * 128u, gv[q], gc[q], g0[q], g1[q]);
               }
             }
           };
