@@ -687,7 +687,9 @@ __global__ void __launch_bounds__(ISECT_MAX_WARPS * 32, 1) isect_kernel(const Is
         // straight-line epilogue with pointers advanced per group, no bounds
         // tests, and the per-query cosine branch hoisted out of the cell loop;
         // kNN votes each group against its bounds instead of storing it
-        constexpr int EP = KPL > 0 ? EPF_KNN : EPF;  // 128-cell groups in flight
+        // 128-cell groups in flight: 2 for kNN and KL (KL's count array makes
+        // each group heavier: C3 KL 11.56 -> 10.74 ms; JS / canberra lose with 2)
+        constexpr int EP = (KPL > 0 || CK == C_KL) ? EPF_KNN : EPF;
         if ((KPL > 0 || vec_out) && nt == TJ && TJ % (EP * 128) == 0) {
           // nz: 0 generic cell, 1 cosine of a non-empty query, 2 the same over
           // scaled postings (no per-cell index statistic at all)
